@@ -1,0 +1,425 @@
+"""bench.py — outer-step throughput of the SparseLoCo hot path on B200.
+
+One step = one SparseLoCo outer step on this rank's FSDP shard (§2.1):
+  slc_compress (Eq. 1: pseudo-gradient, EF, chunk Top-k, 2-bit Q, pack, EF residual)
+  [N > 1: NCCL all-gather of the shard payloads into the peer message, overlapped]
+  slc_outer_update fused (Eq. 2: decode + aggregate R peer payloads + theta update)
+Metric (BASELINE.json): outer-step params/s (whole job) and HBM GB/s (% of roofline).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl slc|reference]
+Under torchrun one process per GPU; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# name -> (layout, R peers, param dtype)
+WORKLOADS = {
+    "llama3.2-1b": ("llama3.2-1b", 8, "f32"),      # BASELINE configs[1]
+    "llama3-8b": ("llama3-8b", 20, "f32"),         # BASELINE configs[2]
+    "covenant-72b": ("covenant-72b", 20, "f32"),   # BASELINE configs[3]
+    "llama2-7b": ("llama2-7b", 20, "f32"),         # BASELINE configs[4] base point
+    "1m": ("1m-2d", 1, "f32"),                     # BASELINE configs[0]
+}
+
+BETA = 0.95
+ALPHA = 1.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--R", type=int, default=None)
+    ap.add_argument("--dtype", default=None, choices=[None, "f32", "bf16"])
+    ap.add_argument("--impl", default="slc", choices=["slc", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peak_hbm():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------- inputs
+class ShardState:
+    """This rank's device buffers: theta (shared global params), theta_local and
+    e of the own peer, and the own records — synthetic, from slcgen."""
+
+    def __init__(self, plan, layout, seed, peer, dtype, warm_ef, records=None):
+        import torch
+        self.plan, self.layout, self.seed, self.peer, self.warm = plan, layout, seed, peer, warm_ef
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        dev = torch.device("cuda", plan.device)
+        n = plan.shard_elems
+        self.theta = torch.zeros(n, dtype=tdt, device=dev)
+        self.theta_local = torch.zeros(n, dtype=tdt, device=dev)
+        self.ef = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.records = records if records is not None else torch.zeros(plan.payload_bytes, dtype=torch.uint8,
+                                                                        device=dev)
+        self.reset()
+
+    def fill(self, buf, what, peer):
+        import numpy as np
+        import slcgen
+        offs = np.cumsum([0] + [int(np.prod(s)) for _, s in self.layout])
+        for s in self.plan.segments:
+            slcgen.fill_cuda(buf[s.shard_offset:s.shard_offset + s.n_elems], what, self.seed, peer,
+                             int(offs[s.tensor]) + s.tensor_begin, warm_ef=self.warm)
+
+    def reset(self, peer=None):
+        import slcgen
+        p = self.peer if peer is None else peer
+        self.fill(self.theta, slcgen.WHAT_THETA, p)
+        self.fill(self.theta_local, slcgen.WHAT_THETA_LOCAL, p)
+        self.fill(self.ef, slcgen.WHAT_EF, p)
+
+
+def make_peer_records(plan, layout, shard, seed, n_peers, first_peer, dtype):
+    """Simulated peers' payload slices for this shard: each peer compresses its
+    own (theta, theta_local_r, e_r) — produced with the same kernel, untimed."""
+    import torch
+    out = []
+    for r in range(first_peer, first_peer + n_peers):
+        shard.reset(peer=r)
+        rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=shard.theta.device)
+        plan.compress(shard.theta, shard.theta_local, shard.ef, rec, beta=BETA)
+        out.append(rec)
+    torch.cuda.synchronize()
+    return out
+
+
+# --------------------------------------------------------------------------- slc arm
+def run_slc(args):
+    import torch
+    import torch.distributed as dist
+
+    import slcgen
+    from paper_2603_08163_b200 import slc
+    from paper_2603_08163_b200 import dist as sdist
+
+    rank, world, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload or ("llama3.2-1b" if world == 1 else "llama3-8b")
+    lname, R, dtype = WORKLOADS[wl]
+    R = args.R or R
+    dtype = args.dtype or dtype
+    layout = slcgen.layouts.LAYOUTS[lname]
+    plan = slc.Plan(layout, rank=rank, nranks=world, dtype=dtype, device=local)
+    gather = sdist.PayloadGather(plan) if world > 1 else None
+    shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=True,
+                       records=gather.alloc_records() if gather else None)
+    peers = make_peer_records(plan, layout, shard, seed=0, n_peers=R - 1, first_peer=1, dtype=dtype)
+    shard.reset()
+    recs = [shard.records[:plan.payload_bytes]] + peers
+
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(i=None):
+        if i is not None:
+            ev[i][0].record(stream)
+        plan.compress(shard.theta, shard.theta_local, shard.ef, shard.records, beta=BETA, stream=stream)
+        if i is not None:
+            ev[i][1].record(stream)
+        if gather is not None:
+            gather.start(shard.records)
+        plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
+        if gather is not None:
+            gather.wait()
+        if i is not None:
+            ev[i][2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = plan.get_status()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = plan.get_status()
+    if st != slc.OK:
+        raise RuntimeError(f"device status {slc.status_string(st)}")
+    ms_total = t0.elapsed_time(t1)
+    ms_compress = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    ms_update = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    t = torch.tensor([ms_total, ms_compress, ms_update], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, ms_compress, ms_update = t.tolist()
+    ms_step = ms_total / args.steps
+
+    info = plan.info
+    P_total = info.total_elems
+    rb = info.record_bytes
+    pb = 4 if dtype == "f32" else 2
+    n_local = sum(s.n_elems for s in plan.segments)
+    # algorithmic bytes: compress reads theta, theta_local, e, writes e + own records;
+    # fused update reads R records + theta, writes theta
+    comp_bytes = n_local * (2 * pb + 8) + info.n_chunks * rb
+    upd_bytes = n_local * 2 * pb + R * info.n_chunks * rb
+    peak, peak_src = peak_hbm()
+    comp_gbs = comp_bytes / (ms_compress * 1e-3) / 1e9
+    step_gbs_rank = (comp_bytes + upd_bytes) / (ms_step * 1e-3) / 1e9
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, plan, shard, recs, stream)
+
+    out = {
+        "metric": "outer-step params/s",
+        "value": P_total / (ms_step * 1e-3),
+        "unit": "params/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if dtype == "f32" else "bf16-params/f32-ef",
+        "data": "synthetic (slcgen: seeded Llama-shaped param sets; random-init values)",
+        "config": {"workload": f"{wl} ({P_total} params), R={R} peers, C=4096 k=64 2-bit, beta={BETA} alpha={ALPHA}",
+                   "params": P_total, "peers": R, "parallelism": f"fsdp-shard{world}",
+                   "l2": "inputs > L2 (126 MB): no flush needed"},
+        "hbm_gbs": step_gbs_rank * world,
+        "hbm_frac_of_peak": step_gbs_rank / peak,
+        "roofline": {"bound": "hbm", "kernel": "slc_compress", "achieved": comp_gbs, "peak": peak,
+                     "unit": "GB/s", "frac": comp_gbs / peak, "traffic": None, "peak_source": peak_src},
+        "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
+                    "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(layout, R, dtype, args.cpu_seconds)
+    if world > 1:
+        dist.destroy_process_group()
+    return out if rank == 0 else None
+
+
+def run_e2e(args, plan, shard, recs, stream):
+    """Same step through the public API with host buffers: every step copies
+    the step's inputs (theta_local, the R-1 peer payloads) from pinned host
+    memory and reads back the own payload (to upload) — copies inside the timer."""
+    import torch
+    n = plan.shard_elems
+    tl_host = torch.empty(n, dtype=shard.theta_local.dtype, pin_memory=True)
+    tl_host.copy_(shard.theta_local)
+    peer_host = [r.cpu().pin_memory() for r in recs[1:]]
+    own_host = torch.empty(plan.payload_bytes, dtype=torch.uint8, pin_memory=True)
+    h2d = tl_host.numel() * tl_host.element_size() + sum(p.numel() for p in peer_host)
+    d2h = own_host.numel()
+    steps = max(2, min(args.steps, 5))
+
+    def step():
+        shard.theta_local.copy_(tl_host, non_blocking=True)
+        for d, h in zip(recs[1:], peer_host):
+            d.copy_(h, non_blocking=True)
+        plan.compress(shard.theta, shard.theta_local, shard.ef, shard.records, beta=BETA, stream=stream)
+        plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
+        own_host.copy_(shard.records, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    return {"value": plan.info.total_elems / (ms * 1e-3) if plan.info.nranks == 1 else
+            plan.info.total_elems / (ms * 1e-3), "unit": "params/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps}
+
+
+# --------------------------------------------------------------------------- oracle (CPU) arm
+def cpu_baseline(layout, R, dtype, seconds):
+    """The oracle as it stands, single-threaded, on a bounded sample of the
+    workload's chunks: compress of the own chunk + R-1 peers' records, then
+    aggregate + update — params/s extrapolated from chunks/s."""
+    import numpy as np
+
+    import oracle
+    import slcgen
+    g = oracle.geom()
+    offs = np.cumsum([0] + [int(np.prod(s)) for _, s in layout])
+    # deterministic sample: every 97th tensor chunk, cycling through tensors
+    chunks = []
+    for ti, (_, shape) in enumerate(layout):
+        nc = oracle.tensor_chunks(shape, g)
+        for c in range(0, nc, max(1, nc // 8)):
+            chunks.append((ti, c))
+    rng = np.random.default_rng(0)
+    rng.shuffle(chunks)
+    done = 0
+    elems = 0
+    t0 = time.perf_counter()
+    work = 0.0
+    for ti, c in chunks:
+        shape = layout[ti][1]
+        off = oracle.chunk_offsets(shape, c, g)
+        G = offs[ti] + off
+        # inputs (generation excluded from timing)
+        ins = []
+        for r in range(R):
+            a = slcgen.generate_at(0, 0, r, G, dtype=dtype)
+            l = slcgen.generate_at(1, 0, r, G, dtype=dtype)
+            e = slcgen.generate_at(2, 0, r, G, warm_ef=True)
+            ins.append((a, l, e))
+        s = time.perf_counter()
+        recs = []
+        for r in range(R):
+            st, rec, en = oracle.compress_chunk(*ins[r], BETA, g)
+            recs.append(rec)
+        delta = oracle.aggregate_chunk(recs, len(off), g=g)
+        oracle.outer_update(ins[0][0], delta, ALPHA)
+        work += time.perf_counter() - s
+        done += 1
+        elems += len(off)
+        if work > seconds or time.perf_counter() - t0 > 4 * seconds:
+            break
+    # per outer step a peer compresses ONE payload (its own) and aggregates R: count 1 compress + 1 aggregate
+    # per chunk -> scale the R compresses down to 1
+    per_elem_s = work / elems
+    comp_share = None
+    # time one compress alone on the last chunk to split the cost
+    s = time.perf_counter()
+    for _ in range(5):
+        oracle.compress_chunk(*ins[0], BETA, g)
+    t_comp = (time.perf_counter() - s) / 5
+    t_chunk_total = work / done
+    t_step_chunk = t_chunk_total - (R - 1) * t_comp
+    v = (elems / done) / t_step_chunk
+    return {"value": v, "unit": "params/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} chunks of {len(layout)} tensors ({elems} params), R={R}, single-threaded C oracle, "
+                      f"{work:.1f}s; per-chunk = 1 compress + aggregate of R records + update"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on host cores."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    wl = args.workload or ("llama3.2-1b" if world == 1 else "llama3-8b")
+    lname, R, dtype = WORKLOADS[wl]
+    R = args.R or R
+    dtype = args.dtype or dtype
+    import slcgen
+    layout = slcgen.layouts.LAYOUTS[lname]
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(layout, R, dtype, per_step)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    P = slcgen.layouts.total_params(layout)
+    return {"impl": "reference", "metric": "outer-step params/s", "value": v, "unit": "params/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": P / v * 1e3,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic (slcgen)",
+            "config": {"workload": f"{wl} ({P} params), R={R} peers, C=4096 k=64 2-bit", "params": P, "peers": R},
+            "cpu_baseline": {"value": v, "unit": "params/s", "cores": 1, "kind": "oracle", "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    out = run_reference(args) if args.impl == "reference" else run_slc(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/* slc.h — C ABI of the B200 (sm_100a) SparseLoCo outer-step hot path.
+ *
+ * Implements, per FSDP shard of one peer, §2.1 (arxiv 2603.08163):
+ *   Eq. 1  Delta_r = theta - theta_r^(t,H);
+ *                    hatDelta_r = Q(Top-k(beta*e_r + Delta_r));
+ *                    e_r <- beta*e_r + Delta_r - hatDelta_r          -> slc_compress
+ *   Eq. 2  Delta = (1/R) sum_r hatDelta_r                   -> slc_decode_aggregate
+ *                    theta <- theta - alpha*Delta                     -> slc_outer_update
+ * with the chunk-wise Top-k of P:88 (64x64 blocks of 2-D tensors, 4096-chunks
+ * of 1-D tensors), C = 4096, k = 64, beta = 0.95, alpha = 1 (0.65 P:180),
+ * 2-bit values and 12-bit fixed-width indices.  Points the
+ * paper leaves open follow DESIGN.md §3 (readings R#1..R#25).
+ *
+ * General conventions
+ *  - Every buffer argument named *_dev is a CUDA DEVICE pointer on the plan's
+ *    device, owned by the caller (the library never frees or retains it).
+ *    Arguments named *_host are host pointers read before the call returns.
+ *  - Compute calls are asynchronous on `stream` (a cudaStream_t passed as
+ *    void*, NULL = legacy default stream), allocate nothing and never
+ *    synchronize.  One plan must not be used on two streams concurrently.
+ *  - Argument / header errors are detected on the host and returned
+ *    synchronously; nothing is launched then.  Data errors found on the device
+ *    (a non-finite theta, theta_local, e or beta*e + Delta; an fp16 scale that
+ *    overflows) are LATCHED in the plan and reported by slc_get_status(); the
+ *    outputs of the offending call are then unspecified.
+ *  - The only allocations are made by slc_plan_create (device chunk table and
+ *    error word) and released by slc_plan_destroy.
+ */
+#ifndef SLC_H
+#define SLC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SLC_OK = 0,
+  SLC_ERR_INVALID_ARGUMENT = 1, /* bad pointer / size / geometry / header field      */
+  SLC_ERR_INVALID_DATA = 2,     /* non-finite input or fp16 scale overflow (latched)  */
+  SLC_ERR_STALE = 3,            /* peer headers disagree: base_round, layout digest, geometry */
+  SLC_ERR_CUDA = 4,             /* a CUDA runtime call failed                         */
+  SLC_ERR_UNSUPPORTED = 5       /* geometry without a compiled kernel                 */
+} slc_status;
+
+typedef enum { SLC_F32 = 0, SLC_BF16 = 1 } slc_dtype; /* dtype of theta / theta_local; e is fp32 */
+
+/* Chunk geometry.  Default {64, 4096, 64, 12}.
+ * Requires chunk == block*block, 1 <= k <= 256, k <= chunk,
+ * 2^index_bits >= chunk, index_bits <= 16.  Compiled chunk sizes: 1024, 4096, 16384. */
+typedef struct {
+  int32_t block;      /* side of a square 2-D chunk                  */
+  int32_t chunk;      /* C, positions per chunk                      */
+  int32_t k;          /* values sent per full chunk                  */
+  int32_t index_bits; /* bits per transmitted in-chunk index         */
+} slc_geometry;
+
+/* One tensor of the GLOBAL parameter layout (row-major, up to 4 dims).  A
+ * 2-D tensor whose dims are both multiples of `block` is cut into blocks in
+ * row-major block order, in-block position p = block*row + col (R#7, R#8);
+ * every other tensor is flattened and cut into C-element chunks, the last one
+ * possibly partial with k_eff = max(1, floor(k*len/C)) (R#9, R#10). */
+typedef struct {
+  int32_t ndim;
+  int64_t dims[4];
+} slc_tensor;
+
+/* What a plan covers (filled by slc_plan_info). */
+typedef struct {
+  int64_t total_elems;   /* parameters in the whole layout                       */
+  int64_t total_chunks;  /* chunks in the whole layout (global chunk order)      */
+  int64_t first_chunk;   /* global index of this shard's first chunk             */
+  int64_t n_chunks;      /* chunks in this shard                                 */
+  int64_t shard_elems;   /* length of this shard's dense buffers, in elements    */
+  int64_t record_bytes;  /* bytes per chunk record (116 at the default geometry) */
+  int64_t payload_bytes; /* n_chunks * record_bytes                              */
+  int32_t n_segments;    /* tensor slices held by this shard                     */
+  int32_t rank, nranks;
+} slc_plan_info;
+
+/* One tensor slice held by a shard (slc_plan_segment).  The shard's dense
+ * buffers (theta, theta_local, e, Delta) are the concatenation of its
+ * segments, each starting at a 64-element (256-byte) aligned shard offset;
+ * the padding between segments is never read or written by the library. */
+typedef struct {
+  int32_t tensor;        /* index into the layout                                        */
+  int32_t blocked;       /* 1: rows x cols slice cut into blocks; 0: flat chunks          */
+  int64_t tensor_begin;  /* first element of the slice in the tensor's row-major order    */
+  int64_t n_elems;       /* elements in the slice (contiguous in that order)              */
+  int64_t shard_offset;  /* element offset of the slice in the shard buffers              */
+  int64_t rows, cols;    /* blocked: slice shape; flat: rows = n_elems, cols = 1          */
+  int64_t first_chunk;   /* global chunk index of the slice's first chunk                 */
+  int64_t n_chunks;
+} slc_segment;
+
+/* Host-side header of one peer's payload slice (SPEC S:99-104 CompressedDelta,
+ * its base-round / peer-id / layout-digest fields).  Optional: pass NULL to
+ * skip the checks. */
+typedef struct {
+  char magic[4];             /* "SLC1"                                        */
+  uint32_t version;          /* 1                                             */
+  slc_geometry geom;
+  uint64_t base_round;       /* outer round the payload was built on          */
+  uint8_t peer_id[16];       /* canonical aggregation order = ascending id    */
+  uint8_t layout_digest[32]; /* slc_layout_digest of the global layout        */
+  int64_t first_chunk;       /* global chunk range of the records described   */
+  int64_t n_chunks;
+} slc_payload_hdr;
+
+typedef struct slc_plan slc_plan;
+
+/* Build the plan of shard `rank` of `nranks` (R#11): the global chunk sequence
+ * (tensors in layout order, chunks in row-major block order) is cut into
+ * nranks contiguous ranges balanced by element count, cutting blocked tensors
+ * only at block-row boundaries ("compression can be performed independently on
+ * each shard"; EF sharded like the inner state).  Uploads the
+ * shard's chunk table to `device`.  Returns INVALID_ARGUMENT for a bad
+ * layout / rank, UNSUPPORTED for a geometry without a kernel, CUDA on a failed
+ * allocation.  *out is NULL on failure. */
+slc_status slc_plan_create(const slc_geometry* geom_host, const slc_tensor* layout_host, int32_t n_tensors,
+                           int32_t rank, int32_t nranks, slc_dtype param_dtype, int32_t device,
+                           slc_plan** out);
+slc_status slc_plan_info_get(const slc_plan* plan, slc_plan_info* out_host);
+slc_status slc_plan_segment(const slc_plan* plan, int32_t i, slc_segment* out_host);
+/* bytes of one chunk record: 4*(ceil(k*index_bits/32) + ceil(2k/32) + 1); -1 on a bad geometry */
+int64_t slc_record_bytes(const slc_geometry* geom_host);
+/* 32-byte digest of (geometry, layout); non-cryptographic (splitmix64 lanes) */
+slc_status slc_layout_digest(const slc_geometry* geom_host, const slc_tensor* layout_host, int32_t n_tensors,
+                             uint8_t out_host[32]);
+
+/* Eq. 1 on the plan's shard, all chunks:
+ *   theta_dev        [shard_elems] param_dtype — theta^(t), the synchronized anchor (read)
+ *   theta_local_dev  [shard_elems] param_dtype — theta_r^(t,H) after H inner steps (read)
+ *   ef_dev           [shard_elems] fp32        — e_r^(t) in, e_r^(t+1) out (in place)
+ *   beta             EF decay (0.95)
+ *   records_dev      [n_chunks * record_bytes] — hatDelta_r of the shard, chunk c of the
+ *                    shard at byte c*record_bytes, 4-byte aligned (R#6 layout)
+ * Per chunk: d = theta - theta_local; b = fma(beta, e, d) (R#12); the k_eff
+ * positions of largest |b|, ties to the lower position (R#3, R#4), ascending
+ * (R#5); 2-bit sign+bucket code with two fp16 bucket-mean scales (R#1, R#13,
+ * R#14); e <- b - dequant (selected) or b (others).  16-byte aligned dense
+ * buffers required.  Latches INVALID_DATA on a non-finite value or an fp16
+ * overflow. */
+slc_status slc_compress(slc_plan* plan, const void* theta_dev, const void* theta_local_dev, float* ef_dev,
+                        float beta, void* records_dev, void* stream);
+
+/* Eq. 2 line 1: agg_dev[shard_elems] (fp32, padding untouched) <-
+ * (1/R) sum_r w_r * decode(records_dev_host[r]) over the shard's chunks.
+ *   hdrs_host          R headers or NULL (then no checks, given order is canonical)
+ *   records_dev_host   host array of R device pointers, each to this shard's
+ *                      n_chunks records of one peer (same layout as slc_compress)
+ *   R                  1 <= R <= 256 (own payload counts as one peer, R#16)
+ *   weights_host       R floats or NULL (= all 1).  With NULL the sum is exact
+ *                      (fixed-point, order-free, R#17); otherwise fp64 in
+ *                      ascending peer-id order (median-norm weights).
+ * Header checks: magic/version/chunk range -> INVALID_ARGUMENT; differing
+ * geometry, base_round or layout_digest -> STALE; duplicate peer ids ->
+ * INVALID_ARGUMENT. */
+slc_status slc_decode_aggregate(slc_plan* plan, const slc_payload_hdr* hdrs_host,
+                                const void* const* records_dev_host, int32_t R, const float* weights_host,
+                                float* agg_dev, void* stream);
+
+/* Eq. 2 line 2: theta <- fma(-alpha, Delta, theta) (R#18) over the shard.
+ *   theta_dev  [shard_elems] param_dtype, in place
+ *   agg_dev    dense fp32 Delta from slc_decode_aggregate, or NULL: then the
+ *              fused kernel decodes and aggregates hdrs/records/R/weights (same
+ *              meaning as above) per chunk and never materialises Delta.
+ *   alpha      outer learning rate (1, later 0.65) */
+slc_status slc_outer_update(slc_plan* plan, void* theta_dev, const float* agg_dev,
+                            const slc_payload_hdr* hdrs_host, const void* const* records_dev_host, int32_t R,
+                            const float* weights_host, float alpha, void* stream);
+
+/* Latched device-side status of the plan.  synchronize != 0: wait for the
+ * plan's device, read and clear the device error word.  synchronize == 0:
+ * return (and clear) what was already latched on the host. */
+slc_status slc_get_status(slc_plan* plan, int32_t synchronize);
+void slc_plan_destroy(slc_plan* plan);
+const char* slc_status_string(slc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLC_H */

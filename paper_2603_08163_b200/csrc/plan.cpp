@@ -1,0 +1,426 @@
+// plan.cpp — host side of libslc: geometry validation, FSDP-style shard
+// partition (R#11), per-chunk table, payload-header checks, error
+// latch and the C-ABI entry points declared in include/slc.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "slc_internal.cuh"
+
+using slc::ChunkDesc;
+
+struct slc_plan {
+  slc_geometry geom;
+  slc::Geom g;
+  slc_dtype dtype;
+  int device;
+  int rank, nranks;
+  std::vector<slc_tensor> layout;
+  std::vector<slc_segment> segs;
+  int64_t total_elems = 0, total_chunks = 0, first_chunk = 0, n_chunks = 0, shard_elems = 0;
+  ChunkDesc* d_chunks = nullptr;
+  uint32_t* d_err = nullptr;
+  slc_status latched = SLC_OK;
+  uint8_t digest[32];
+};
+
+namespace {
+
+int64_t numel(const slc_tensor& t) {
+  int64_t n = 1;
+  for (int i = 0; i < t.ndim; i++) n *= t.dims[i];
+  return n;
+}
+
+bool blocked(const slc_tensor& t, int B) { return t.ndim == 2 && t.dims[0] % B == 0 && t.dims[1] % B == 0; }
+
+int64_t tensor_chunks(const slc_tensor& t, const slc_geometry& g) {
+  if (blocked(t, g.block)) return (t.dims[0] / g.block) * (t.dims[1] / g.block);
+  return (numel(t) + g.chunk - 1) / g.chunk;
+}
+
+slc_status check_geom(const slc_geometry* g) {
+  if (!g) return SLC_ERR_INVALID_ARGUMENT;
+  if (g->block <= 0 || g->block > 1024 || g->chunk != g->block * g->block) return SLC_ERR_INVALID_ARGUMENT;
+  if (g->k < 1 || g->k > g->chunk || g->k > slc::kMaxK) return SLC_ERR_INVALID_ARGUMENT;
+  if (g->index_bits < 1 || g->index_bits > 16 || (1L << g->index_bits) < g->chunk) return SLC_ERR_INVALID_ARGUMENT;
+  return SLC_OK;
+}
+
+slc::Geom make_geom(const slc_geometry& g) {
+  slc::Geom r;
+  r.B = g.block;
+  r.C = g.chunk;
+  r.k = g.k;
+  r.ib = g.index_bits;
+  r.idx_words = (g.k * g.index_bits + 31) / 32;
+  r.code_words = (2 * g.k + 31) / 32;
+  r.rec_words = r.idx_words + r.code_words + 1;
+  return r;
+}
+
+uint64_t mix64(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27; z *= 0x94D049BB133111EBull; z ^= z >> 31;
+  return z;
+}
+
+void digest_of(const slc_geometry& g, const slc_tensor* lay, int n, uint8_t out[32]) {
+  uint64_t h[4] = {0x5EED0001ull, 0x5EED0002ull, 0x5EED0003ull, 0x5EED0004ull};
+  auto feed = [&](uint64_t v) {
+    for (int i = 0; i < 4; i++) h[i] = mix64(h[i] ^ (v + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1)));
+  };
+  feed((uint64_t)g.block); feed((uint64_t)g.chunk); feed((uint64_t)g.k); feed((uint64_t)g.index_bits);
+  feed((uint64_t)n);
+  for (int t = 0; t < n; t++) {
+    feed((uint64_t)lay[t].ndim);
+    for (int d = 0; d < lay[t].ndim; d++) feed((uint64_t)lay[t].dims[d]);
+  }
+  for (int i = 0; i < 4; i++)
+    for (int b = 0; b < 8; b++) out[8 * i + b] = (uint8_t)(h[i] >> (8 * b));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Partition (R#11): cut points are element positions in the global flat order
+// that fall on unit boundaries (unit = block-row of a blocked tensor, chunk of
+// a flat tensor), each the boundary nearest to g*total/nranks.
+std::vector<int64_t> cut_points(const std::vector<slc_tensor>& lay, const slc_geometry& g, int nranks,
+                                int64_t total) {
+  std::vector<int64_t> cuts(nranks + 1, 0);
+  cuts[nranks] = total;
+  for (int r = 1; r < nranks; r++) {
+    const long double target = (long double)total * r / nranks;
+    int64_t best = 0;
+    long double best_d = -1;
+    int64_t off = 0;
+    for (const auto& t : lay) {
+      const int64_t n = numel(t);
+      if (target >= off && target <= off + n) {
+        int64_t unit = blocked(t, g.block) ? (int64_t)g.block * t.dims[1] : (int64_t)g.chunk;
+        int64_t i = (int64_t)((target - off) / unit);
+        for (int64_t cand_i : {i, i + 1}) {
+          int64_t pos = off + std::min(cand_i * unit, n);
+          long double d = pos > target ? pos - target : target - pos;
+          if (best_d < 0 || d < best_d) { best_d = d; best = pos; }
+        }
+      }
+      off += n;
+    }
+    cuts[r] = best;
+  }
+  for (int r = 1; r <= nranks; r++) cuts[r] = std::max(cuts[r], cuts[r - 1]);
+  return cuts;
+}
+
+slc_status header_checks(const slc_plan* p, const slc_payload_hdr* h, int R, std::vector<int>& order) {
+  order.resize(R);
+  for (int r = 0; r < R; r++) order[r] = r;
+  if (!h) return SLC_OK;
+  for (int r = 0; r < R; r++) {
+    if (std::memcmp(h[r].magic, "SLC1", 4) != 0 || h[r].version != 1) return SLC_ERR_INVALID_ARGUMENT;
+    if (h[r].first_chunk != p->first_chunk || h[r].n_chunks != p->n_chunks) return SLC_ERR_INVALID_ARGUMENT;
+    if (std::memcmp(&h[r].geom, &p->geom, sizeof(slc_geometry)) != 0) return SLC_ERR_STALE;
+    if (std::memcmp(h[r].layout_digest, p->digest, 32) != 0) return SLC_ERR_STALE;
+    if (h[r].base_round != h[0].base_round) return SLC_ERR_STALE;
+  }
+  std::sort(order.begin(), order.end(),
+            [&](int a, int b) { return std::memcmp(h[a].peer_id, h[b].peer_id, 16) < 0; });
+  for (int i = 1; i < R; i++)
+    if (std::memcmp(h[order[i - 1]].peer_id, h[order[i]].peer_id, 16) == 0) return SLC_ERR_INVALID_ARGUMENT;
+  return SLC_OK;
+}
+
+slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int R, const float* w,
+                    slc::AggArgs& a) {
+  if (R < 1 || R > slc::kMaxPeers || !recs) return SLC_ERR_INVALID_ARGUMENT;
+  std::vector<int> order;
+  slc_status st = header_checks(p, hdrs, R, order);
+  if (st != SLC_OK) return st;
+  std::memset(&a, 0, sizeof(a));
+  a.chunks = p->d_chunks;
+  a.n_chunks = p->n_chunks;
+  a.R = R;
+  a.weighted = w != nullptr;
+  a.invR = 1.0 / (double)R;
+  a.err = p->d_err;
+  a.g = p->g;
+  for (int i = 0; i < R; i++) {
+    const int r = order[i];  // canonical order (matters only when weighted)
+    if (!recs[r] && p->n_chunks > 0) return SLC_ERR_INVALID_ARGUMENT;
+    if (((uintptr_t)recs[r]) & 3u) return SLC_ERR_INVALID_ARGUMENT;
+    a.rec[i] = static_cast<const uint32_t*>(recs[r]);
+    a.w[i] = w ? w[r] : 1.0f;
+  }
+  return SLC_OK;
+}
+
+slc_status cuda_status(cudaError_t e, slc_plan* p) {
+  if (e == cudaSuccess) return SLC_OK;
+  p->latched = SLC_ERR_CUDA;
+  return SLC_ERR_CUDA;
+}
+
+bool aligned16(const void* q) { return (((uintptr_t)q) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int64_t slc_record_bytes(const slc_geometry* g) {
+  if (check_geom(g) != SLC_OK) return -1;
+  return 4 * (int64_t)make_geom(*g).rec_words;
+}
+
+slc_status slc_layout_digest(const slc_geometry* g, const slc_tensor* lay, int32_t n, uint8_t out[32]) {
+  if (check_geom(g) != SLC_OK || !lay || n < 1 || !out) return SLC_ERR_INVALID_ARGUMENT;
+  digest_of(*g, lay, n, out);
+  return SLC_OK;
+}
+
+slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, int32_t n_tensors, int32_t rank,
+                           int32_t nranks, slc_dtype dtype, int32_t device, slc_plan** out) {
+  if (!out) return SLC_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  slc_status st = check_geom(geom);
+  if (st != SLC_OK) return st;
+  if (!layout || n_tensors < 1 || nranks < 1 || rank < 0 || rank >= nranks) return SLC_ERR_INVALID_ARGUMENT;
+  if (dtype != SLC_F32 && dtype != SLC_BF16) return SLC_ERR_INVALID_ARGUMENT;
+  if (!slc::compress_supported(geom->chunk)) return SLC_ERR_UNSUPPORTED;
+  for (int t = 0; t < n_tensors; t++) {
+    if (layout[t].ndim < 1 || layout[t].ndim > 4) return SLC_ERR_INVALID_ARGUMENT;
+    for (int d = 0; d < layout[t].ndim; d++)
+      if (layout[t].dims[d] < 1) return SLC_ERR_INVALID_ARGUMENT;
+    if (blocked(layout[t], geom->block) && layout[t].dims[1] > INT32_MAX) return SLC_ERR_INVALID_ARGUMENT;
+  }
+
+  slc_plan* p = new (std::nothrow) slc_plan();
+  if (!p) return SLC_ERR_INVALID_ARGUMENT;
+  p->geom = *geom;
+  p->g = make_geom(*geom);
+  p->dtype = dtype;
+  p->device = device;
+  p->rank = rank;
+  p->nranks = nranks;
+  p->layout.assign(layout, layout + n_tensors);
+  digest_of(*geom, layout, n_tensors, p->digest);
+
+  for (const auto& t : p->layout) {
+    p->total_elems += numel(t);
+    p->total_chunks += tensor_chunks(t, *geom);
+  }
+  const std::vector<int64_t> cuts = cut_points(p->layout, *geom, nranks, p->total_elems);
+  const int64_t lo = cuts[rank], hi = cuts[rank + 1];
+
+  // segments of [lo, hi) and the chunk table
+  std::vector<ChunkDesc> table;
+  int64_t off = 0, chunk0 = 0, shard_off = 0;
+  bool first_set = false;
+  for (int ti = 0; ti < n_tensors; ti++) {
+    const slc_tensor& t = p->layout[ti];
+    const int64_t n = numel(t), nc = tensor_chunks(t, *geom);
+    const int64_t b = std::max(lo, off), e = std::min(hi, off + n);
+    if (b < e) {
+      slc_segment s;
+      std::memset(&s, 0, sizeof(s));
+      s.tensor = ti;
+      s.blocked = blocked(t, geom->block);
+      s.tensor_begin = b - off;
+      s.n_elems = e - b;
+      s.shard_offset = (shard_off + 63) / 64 * 64;
+      const int64_t B = geom->block, C = geom->chunk;
+      if (s.blocked) {
+        const int64_t cols = t.dims[1], nb = cols / B;
+        const int64_t r0 = s.tensor_begin / cols, r1 = (s.tensor_begin + s.n_elems) / cols;
+        s.rows = r1 - r0;
+        s.cols = cols;
+        s.first_chunk = chunk0 + (r0 / B) * nb;
+        s.n_chunks = (s.rows / B) * nb;
+        for (int64_t bi = 0; bi < s.rows / B; bi++)
+          for (int64_t bj = 0; bj < nb; bj++)
+            table.push_back(ChunkDesc{s.shard_offset + bi * B * cols + bj * B, (int32_t)cols, (int32_t)C});
+      } else {
+        s.rows = s.n_elems;
+        s.cols = 1;
+        const int64_t c_first = s.tensor_begin / C;
+        s.first_chunk = chunk0 + c_first;
+        s.n_chunks = (s.n_elems + C - 1) / C;
+        for (int64_t c = 0; c < s.n_chunks; c++) {
+          const int64_t len = std::min(C, s.n_elems - c * C);
+          table.push_back(ChunkDesc{s.shard_offset + c * C, 0, (int32_t)len});
+        }
+      }
+      if (!first_set) { p->first_chunk = s.first_chunk; first_set = true; }
+      shard_off = s.shard_offset + s.n_elems;
+      p->segs.push_back(s);
+    }
+    off += n;
+    chunk0 += nc;
+  }
+  if (!first_set) {  // empty shard: first_chunk = chunks before lo
+    int64_t c = 0, o = 0;
+    for (const auto& t : p->layout) {
+      if (o >= lo) break;
+      c += tensor_chunks(t, *geom);
+      o += numel(t);
+    }
+    p->first_chunk = c;
+  }
+  p->n_chunks = (int64_t)table.size();
+  p->shard_elems = shard_off;
+
+  if (device < 0) {  // host-only plan: geometry / partition queries, no compute
+    *out = p;
+    return SLC_OK;
+  }
+  DeviceGuard guard(device);
+  cudaError_t ce = cudaMalloc(&p->d_err, sizeof(uint32_t));
+  if (ce == cudaSuccess) ce = cudaMemset(p->d_err, 0, sizeof(uint32_t));
+  if (ce == cudaSuccess && !table.empty()) {
+    ce = cudaMalloc(&p->d_chunks, table.size() * sizeof(ChunkDesc));
+    if (ce == cudaSuccess)
+      ce = cudaMemcpy(p->d_chunks, table.data(), table.size() * sizeof(ChunkDesc), cudaMemcpyHostToDevice);
+  }
+  if (ce != cudaSuccess) {
+    if (p->d_err) cudaFree(p->d_err);
+    if (p->d_chunks) cudaFree(p->d_chunks);
+    delete p;
+    cudaGetLastError();
+    return SLC_ERR_CUDA;
+  }
+  *out = p;
+  return SLC_OK;
+}
+
+slc_status slc_plan_info_get(const slc_plan* p, slc_plan_info* o) {
+  if (!p || !o) return SLC_ERR_INVALID_ARGUMENT;
+  o->total_elems = p->total_elems;
+  o->total_chunks = p->total_chunks;
+  o->first_chunk = p->first_chunk;
+  o->n_chunks = p->n_chunks;
+  o->shard_elems = p->shard_elems;
+  o->record_bytes = 4 * (int64_t)p->g.rec_words;
+  o->payload_bytes = o->record_bytes * p->n_chunks;
+  o->n_segments = (int32_t)p->segs.size();
+  o->rank = p->rank;
+  o->nranks = p->nranks;
+  return SLC_OK;
+}
+
+slc_status slc_plan_segment(const slc_plan* p, int32_t i, slc_segment* o) {
+  if (!p || !o || i < 0 || i >= (int32_t)p->segs.size()) return SLC_ERR_INVALID_ARGUMENT;
+  *o = p->segs[i];
+  return SLC_OK;
+}
+
+slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local, float* ef, float beta,
+                        void* records, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!theta || !theta_local || !ef || !records) return SLC_ERR_INVALID_ARGUMENT;
+  if (!aligned16(theta) || !aligned16(theta_local) || !aligned16(ef) || (((uintptr_t)records) & 3u))
+    return SLC_ERR_INVALID_ARGUMENT;
+  slc::CompressArgs a;
+  a.chunks = p->d_chunks;
+  a.n_chunks = p->n_chunks;
+  a.theta = theta;
+  a.theta_local = theta_local;
+  a.ef = ef;
+  a.records = static_cast<uint32_t*>(records);
+  a.err = p->d_err;
+  a.beta = beta;
+  a.g = p->g;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_compress(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_decode_aggregate(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
+                                const float* w, float* agg, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  slc_status st = prep_agg(p, hdrs, recs, R, w, a);
+  if (st != SLC_OK) return st;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!agg || !aligned16(agg)) return SLC_ERR_INVALID_ARGUMENT;
+  a.mode = slc::kAggOnly;
+  a.agg = agg;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_outer_update(slc_plan* p, void* theta, const float* agg, const slc_payload_hdr* hdrs,
+                            const void* const* recs, int32_t R, const float* w, float alpha, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  if (agg) {
+    std::memset(&a, 0, sizeof(a));
+    a.chunks = p->d_chunks;
+    a.n_chunks = p->n_chunks;
+    a.g = p->g;
+    a.err = p->d_err;
+    a.mode = slc::kUpdateFromAgg;
+    a.agg = const_cast<float*>(agg);
+    if (p->n_chunks > 0 && !aligned16(agg)) return SLC_ERR_INVALID_ARGUMENT;
+  } else {
+    slc_status st = prep_agg(p, hdrs, recs, R, w, a);
+    if (st != SLC_OK) return st;
+    a.mode = slc::kFused;
+  }
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!theta || !aligned16(theta)) return SLC_ERR_INVALID_ARGUMENT;
+  a.alpha = alpha;
+  a.theta = theta;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_get_status(slc_plan* p, int32_t synchronize) {
+  if (!p) return SLC_ERR_INVALID_ARGUMENT;
+  slc_status st = p->latched;
+  p->latched = SLC_OK;
+  if (synchronize && p->device >= 0) {
+    DeviceGuard guard(p->device);
+    uint32_t err = 0;
+    cudaError_t ce = cudaDeviceSynchronize();
+    if (ce == cudaSuccess) ce = cudaMemcpy(&err, p->d_err, sizeof(err), cudaMemcpyDeviceToHost);
+    if (ce == cudaSuccess) ce = cudaMemset(p->d_err, 0, sizeof(uint32_t));
+    if (ce != cudaSuccess) return SLC_ERR_CUDA;
+    if (err && st == SLC_OK) st = SLC_ERR_INVALID_DATA;
+  }
+  return st;
+}
+
+void slc_plan_destroy(slc_plan* p) {
+  if (!p) return;
+  if (p->device >= 0) {
+    DeviceGuard guard(p->device);
+    if (p->d_chunks) cudaFree(p->d_chunks);
+    if (p->d_err) cudaFree(p->d_err);
+  }
+  delete p;
+}
+
+const char* slc_status_string(slc_status s) {
+  switch (s) {
+    case SLC_OK: return "ok";
+    case SLC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SLC_ERR_INVALID_DATA: return "invalid data (non-finite input or fp16 scale overflow)";
+    case SLC_ERR_STALE: return "stale submission (base round / layout digest / geometry mismatch)";
+    case SLC_ERR_CUDA: return "CUDA runtime error";
+    case SLC_ERR_UNSUPPORTED: return "unsupported geometry";
+  }
+  return "unknown status";
+}
+
+}  // extern "C"

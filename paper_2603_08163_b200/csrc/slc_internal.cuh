@@ -1,0 +1,69 @@
+// slc_internal.cuh — shared declarations of libslc (host plan + CUDA kernels).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/slc.h"
+
+namespace slc {
+
+constexpr int kMaxPeers = 256;
+constexpr int kMaxK = 256;
+
+// One chunk of the shard: dense position p of the chunk lives at shard element
+//   base + (p / B) * ld + (p % B)   (blocked, ld = tensor cols)
+//   base + p                        (flat,    ld = 0)
+// len = number of positions (C, or less for the last chunk of a flat tensor).
+struct __align__(16) ChunkDesc {
+  int64_t base;
+  int32_t ld;
+  int32_t len;
+};
+static_assert(sizeof(ChunkDesc) == 16, "ChunkDesc must be 16 bytes");
+
+// Error bits latched on the device.
+enum : uint32_t { kErrNonFinite = 1u, kErrScaleOverflow = 2u };
+
+struct Geom {
+  int B, C, k, ib;
+  int idx_words, code_words, rec_words;
+};
+
+struct CompressArgs {
+  const ChunkDesc* chunks;
+  int64_t n_chunks;
+  const void* theta;
+  const void* theta_local;
+  float* ef;
+  uint32_t* records;
+  uint32_t* err;
+  float beta;
+  Geom g;
+};
+
+enum AggMode : int { kAggOnly = 0, kUpdateFromAgg = 1, kFused = 2 };
+
+struct AggArgs {
+  const ChunkDesc* chunks;
+  int64_t n_chunks;
+  const uint32_t* rec[kMaxPeers];  // per peer: this shard's records
+  float w[kMaxPeers];              // per peer weight (weighted mode only)
+  int R;
+  int weighted;
+  int mode;
+  float alpha;
+  double invR;
+  float* agg;     // kAggOnly: out; kUpdateFromAgg: in
+  void* theta;    // kUpdateFromAgg / kFused: in-out
+  uint32_t* err;
+  Geom g;
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);
+cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
+bool compress_supported(int C);
+
+}  // namespace slc

@@ -1,0 +1,105 @@
+"""One-process-per-GPU harness: the two exchange steps of the path that cross
+GPUs, done with NCCL through torch.distributed (BASELINE.json north_star: "NCCL
+over NVLink is used only to all-gather each GPU's compressed shard payload
+into the peer message, and to exchange simulated peers' payloads").
+
+* a8, PayloadGather — the FSDP shards of one peer each compress their own chunk
+  range; the peer message (what the paper uploads to R2,
+  P:139-145) is the concatenation of the shard payloads in rank order, i.e. in
+  global chunk order.  Shard payload sizes differ by a few chunks, so every
+  rank's records buffer is padded to the largest shard payload and one
+  ncclAllGather moves them; rank g's part sits at byte g*slot of the gathered
+  buffer.  The gather runs on NCCL's stream and overlaps the fused
+  aggregate/update kernel, which only needs the rank's own slices.
+* a9, PeerExchange — stand-in for the R2 download: peer r's full
+  message sits on rank r % n "as if downloaded"; grouped send/recv hands every
+  rank its contiguous slice of every message.  Reported separately.
+
+No dense tensor ever crosses NVLink.  Works with the gloo backend on CPU
+tensors too (tests/test_dist_cpu.py).
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import slc
+
+
+def shard_payloads(layout, geom, nranks: int, dtype: str = "f32") -> List[int]:
+    """Payload bytes of every rank's shard (host-only plans, no device work)."""
+    return [slc.Plan(layout, geom=geom, rank=r, nranks=nranks, dtype=dtype, device=-1).payload_bytes
+            for r in range(nranks)]
+
+
+class PayloadGather:
+    """a8: all-gather of the shard payloads into the peer message."""
+
+    def __init__(self, plan: slc.Plan, group=None, device=None):
+        self.plan = plan
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.sizes = shard_payloads(plan.layout, plan.geom, self.world, plan.dtype)
+        self.slot = max(self.sizes)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.message = torch.zeros(self.world * self.slot, dtype=torch.uint8, device=dev)
+        self._work = None
+
+    def alloc_records(self, device=None) -> torch.Tensor:
+        """Own records buffer, padded to the gather slot."""
+        dev = device if device is not None else self.message.device
+        return torch.zeros(self.slot, dtype=torch.uint8, device=dev)
+
+    def start(self, records: torch.Tensor):
+        assert records.numel() == self.slot, "records must come from alloc_records()"
+        self._work = dist.all_gather_into_tensor(self.message, records, group=self.group, async_op=True)
+
+    def wait(self):
+        if self._work is not None:
+            self._work.wait()
+            self._work = None
+
+    def contiguous_message(self) -> torch.Tensor:
+        """The peer message in global chunk order without the padding."""
+        return torch.cat([self.message[g * self.slot:g * self.slot + self.sizes[g]] for g in range(self.world)])
+
+    def slice_of(self, message: torch.Tensor, g: int) -> torch.Tensor:
+        return message[g * self.slot:g * self.slot + self.sizes[g]]
+
+
+class PeerExchange:
+    """a9: peer r's (padded) message lives on rank r % n; every rank receives
+    its own slice of every message.  Returns per-peer slice buffers."""
+
+    def __init__(self, gather: PayloadGather, n_peers: int):
+        self.g = gather
+        self.n_peers = n_peers
+        dev = gather.message.device
+        self.slices = [torch.zeros(gather.slot, dtype=torch.uint8, device=dev) for _ in range(n_peers)]
+
+    def owner(self, r: int) -> int:
+        return r % self.g.world
+
+    def run(self, owned_messages: Sequence[torch.Tensor]):
+        """owned_messages[i] = full padded message of peer r = rank + i*world."""
+        world, rank, slot = self.g.world, self.g.rank, self.g.slot
+        ops = []
+        for r in range(self.n_peers):
+            o = self.owner(r)
+            if o == rank:
+                msg = owned_messages[r // world]
+                for dst in range(world):
+                    part = msg[dst * slot:(dst + 1) * slot]
+                    if dst == rank:
+                        self.slices[r].copy_(part)
+                    else:
+                        ops.append(dist.P2POp(dist.isend, part, dst, group=self.g.group))
+            else:
+                ops.append(dist.P2POp(dist.irecv, self.slices[r], o, group=self.g.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return [s[:self.g.sizes[rank]] for s in self.slices]

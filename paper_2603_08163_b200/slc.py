@@ -1,0 +1,275 @@
+"""Thin ctypes binding of include/slc.h (libslc.so) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this
+module converts torch tensors / Python values to pointers and sizes and
+raises on a non-OK status.  There is no fallback: if libslc.so is missing the
+import-time load fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libslc.so")
+
+OK, INVALID_ARGUMENT, INVALID_DATA, STALE, CUDA_ERROR, UNSUPPORTED = range(6)
+F32, BF16 = 0, 1
+MAX_PEERS = 256
+
+
+class SlcError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} (status {status})")
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [("block", ctypes.c_int32), ("chunk", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("index_bits", ctypes.c_int32)]
+
+
+class Tensor(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("dims", ctypes.c_int64 * 4)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("total_elems", ctypes.c_int64), ("total_chunks", ctypes.c_int64),
+                ("first_chunk", ctypes.c_int64), ("n_chunks", ctypes.c_int64),
+                ("shard_elems", ctypes.c_int64), ("record_bytes", ctypes.c_int64),
+                ("payload_bytes", ctypes.c_int64), ("n_segments", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("tensor", ctypes.c_int32), ("blocked", ctypes.c_int32), ("tensor_begin", ctypes.c_int64),
+                ("n_elems", ctypes.c_int64), ("shard_offset", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("cols", ctypes.c_int64), ("first_chunk", ctypes.c_int64), ("n_chunks", ctypes.c_int64)]
+
+
+class PayloadHdr(ctypes.Structure):
+    _fields_ = [("magic", ctypes.c_char * 4), ("version", ctypes.c_uint32), ("geom", Geometry),
+                ("base_round", ctypes.c_uint64), ("peer_id", ctypes.c_uint8 * 16),
+                ("layout_digest", ctypes.c_uint8 * 32), ("first_chunk", ctypes.c_int64),
+                ("n_chunks", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: the CUDA extension must be built "
+                           "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    pp = ctypes.POINTER
+    sig = {
+        "slc_plan_create": (ctypes.c_int, [pp(Geometry), pp(Tensor), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int, ctypes.c_int32, pp(P)]),
+        "slc_plan_info_get": (ctypes.c_int, [P, pp(PlanInfo)]),
+        "slc_plan_segment": (ctypes.c_int, [P, ctypes.c_int32, pp(Segment)]),
+        "slc_record_bytes": (ctypes.c_int64, [pp(Geometry)]),
+        "slc_layout_digest": (ctypes.c_int, [pp(Geometry), pp(Tensor), ctypes.c_int32, P]),
+        "slc_compress": (ctypes.c_int, [P, P, P, P, ctypes.c_float, P, P]),
+        "slc_decode_aggregate": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
+        "slc_outer_update": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
+        "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
+        "slc_plan_destroy": (None, [P]),
+        "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+_lib = _load()
+
+EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_record_bytes", "slc_layout_digest",
+            "slc_compress", "slc_decode_aggregate", "slc_outer_update", "slc_get_status", "slc_plan_destroy",
+            "slc_status_string"]
+
+
+def status_string(s: int) -> str:
+    return _lib.slc_status_string(int(s)).decode()
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise SlcError(st, what)
+
+
+def geometry(block: int = 64, k: int = 64, index_bits: Optional[int] = None) -> Geometry:
+    C = block * block
+    ib = index_bits if index_bits is not None else max(1, (C - 1).bit_length())
+    return Geometry(block, C, k, ib)
+
+
+def _layout_array(layout: Sequence[Tuple[str, Tuple[int, ...]]]):
+    arr = (Tensor * len(layout))()
+    for i, (_, shape) in enumerate(layout):
+        if not 1 <= len(shape) <= 4:
+            raise ValueError(f"tensor {i}: {len(shape)} dims")
+        arr[i].ndim = len(shape)
+        for j, s in enumerate(shape):
+            arr[i].dims[j] = int(s)
+    return arr
+
+
+def record_bytes(geom: Geometry) -> int:
+    return int(_lib.slc_record_bytes(ctypes.byref(geom)))
+
+
+def layout_digest(geom: Geometry, layout) -> bytes:
+    arr = _layout_array(layout)
+    out = (ctypes.c_uint8 * 32)()
+    _check(_lib.slc_layout_digest(ctypes.byref(geom), arr, len(layout), out), "slc_layout_digest")
+    return bytes(out)
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+def _dptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class SegmentInfo:
+    tensor: int
+    blocked: bool
+    tensor_begin: int
+    n_elems: int
+    shard_offset: int
+    rows: int
+    cols: int
+    first_chunk: int
+    n_chunks: int
+
+
+def make_header(plan: "Plan", peer_id: bytes, base_round: int = 0) -> PayloadHdr:
+    h = PayloadHdr()
+    h.magic = b"SLC1"
+    h.version = 1
+    h.geom = plan.geom
+    h.base_round = base_round
+    pid = bytes(peer_id)[:16].ljust(16, b"\0")
+    for i in range(16):
+        h.peer_id[i] = pid[i]
+    for i, b in enumerate(plan.digest):
+        h.layout_digest[i] = b
+    h.first_chunk = plan.info.first_chunk
+    h.n_chunks = plan.info.n_chunks
+    return h
+
+
+class Plan:
+    """slc_plan of shard `rank` of `nranks` of a global layout.  device < 0 ->
+    host-only plan (geometry / partition queries, no compute)."""
+
+    def __init__(self, layout, geom: Optional[Geometry] = None, rank: int = 0, nranks: int = 1,
+                 dtype: str = "f32", device: int = 0):
+        self.layout = list(layout)
+        self.geom = geom if geom is not None else geometry()
+        self.dtype = dtype
+        self.device = device
+        arr = _layout_array(self.layout)
+        h = ctypes.c_void_p()
+        _check(_lib.slc_plan_create(ctypes.byref(self.geom), arr, len(self.layout), rank, nranks,
+                                    BF16 if dtype == "bf16" else F32, device, ctypes.byref(h)), "slc_plan_create")
+        self._h = h
+        info = PlanInfo()
+        _check(_lib.slc_plan_info_get(h, ctypes.byref(info)), "slc_plan_info_get")
+        self.info = info
+        self.digest = layout_digest(self.geom, self.layout)
+        self.segments: List[SegmentInfo] = []
+        for i in range(info.n_segments):
+            s = Segment()
+            _check(_lib.slc_plan_segment(h, i, ctypes.byref(s)), "slc_plan_segment")
+            self.segments.append(SegmentInfo(s.tensor, bool(s.blocked), s.tensor_begin, s.n_elems, s.shard_offset,
+                                             s.rows, s.cols, s.first_chunk, s.n_chunks))
+
+    # ---- shape helpers
+    @property
+    def shard_elems(self) -> int:
+        return self.info.shard_elems
+
+    @property
+    def n_chunks(self) -> int:
+        return self.info.n_chunks
+
+    @property
+    def record_bytes(self) -> int:
+        return self.info.record_bytes
+
+    @property
+    def payload_bytes(self) -> int:
+        return self.info.payload_bytes
+
+    # ---- the three calls of the hot path
+    def compress(self, theta, theta_local, ef, records, beta: float = 0.95, stream=None) -> None:
+        """Eq. 1.  theta/theta_local: [shard_elems] f32|bf16, ef: [shard_elems] f32 (in place),
+        records: [payload_bytes] uint8 (or any 4-byte aligned buffer of that size)."""
+        self._check_dense(theta, theta_local, ef)
+        assert records.numel() * records.element_size() >= self.payload_bytes
+        _check(_lib.slc_compress(self._h, _dptr(theta), _dptr(theta_local), _dptr(ef), ctypes.c_float(beta),
+                                 _dptr(records), _stream_ptr(stream)), "slc_compress")
+
+    def _peer_args(self, records: Sequence, hdrs, weights):
+        R = len(records)
+        if not 1 <= R <= MAX_PEERS:
+            raise ValueError(f"R={R}")
+        ptrs = (ctypes.c_void_p * R)(*[r.data_ptr() for r in records])
+        h = None
+        if hdrs is not None:
+            h = (PayloadHdr * R)(*hdrs)
+        w = None
+        if weights is not None:
+            w = (ctypes.c_float * R)(*[float(x) for x in weights])
+        return R, ptrs, h, w
+
+    def decode_aggregate(self, records: Sequence, agg, hdrs=None, weights=None, stream=None) -> None:
+        """Eq. 2 line 1: agg[shard_elems] f32 <- (1/R) sum_r w_r decode(records[r])."""
+        R, ptrs, h, w = self._peer_args(records, hdrs, weights)
+        _check(_lib.slc_decode_aggregate(self._h, h, ptrs, R, w, _dptr(agg), _stream_ptr(stream)),
+               "slc_decode_aggregate")
+
+    def outer_update(self, theta, alpha: float = 1.0, agg=None, records: Optional[Sequence] = None, hdrs=None,
+                     weights=None, stream=None) -> None:
+        """Eq. 2 line 2: theta <- theta - alpha * Delta; agg=None -> fused decode/aggregate/update."""
+        if agg is not None:
+            _check(_lib.slc_outer_update(self._h, _dptr(theta), _dptr(agg), None, None, 0, None,
+                                         ctypes.c_float(alpha), _stream_ptr(stream)), "slc_outer_update")
+        else:
+            R, ptrs, h, w = self._peer_args(records, hdrs, weights)
+            _check(_lib.slc_outer_update(self._h, _dptr(theta), None, h, ptrs, R, w, ctypes.c_float(alpha),
+                                         _stream_ptr(stream)), "slc_outer_update")
+
+    def get_status(self, synchronize: bool = True) -> int:
+        return int(_lib.slc_get_status(self._h, 1 if synchronize else 0))
+
+    def check(self) -> None:
+        _check(self.get_status(True), "device status")
+
+    def _check_dense(self, *ts):
+        for t in ts:
+            if t.numel() < self.shard_elems:
+                raise ValueError(f"dense buffer has {t.numel()} < {self.shard_elems} elements")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.slc_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

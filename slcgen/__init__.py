@@ -11,7 +11,7 @@ import ctypes
 import os
 
 from .gen import (WHAT_EF, WHAT_THETA, WHAT_THETA_LOCAL, FAMILY_NAMES, N_FAMILIES,  # noqa: F401
-                  f32_to_bf16_bits, generate, special_family)
+                  f32_to_bf16_bits, generate, generate_at, special_family)
 from . import layouts  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -183,7 +183,15 @@ def generate(what: int, seed: int, peer: int, G0: int, n: int, *, rowlen: int = 
              special_period: int = 0, warm_ef: bool = False, dtype: str = "f32") -> np.ndarray:
     """Values of `what` for global indices [G0, G0+n).  dtype 'f32' -> float32,
     'bf16' -> uint16 bit patterns (round-to-nearest-even; only theta/theta_local)."""
-    G = np.arange(G0, G0 + n, dtype=np.uint64)
+    return generate_at(what, seed, peer, np.arange(G0, G0 + n, dtype=np.uint64), rowlen=rowlen,
+                       special_period=special_period, warm_ef=warm_ef, dtype=dtype)
+
+
+def generate_at(what: int, seed: int, peer: int, G, *, rowlen: int = 64, special_period: int = 0,
+                warm_ef: bool = False, dtype: str = "f32") -> np.ndarray:
+    """Values of `what` at an arbitrary array of global indices G."""
+    G = np.ascontiguousarray(G, dtype=np.uint64).reshape(-1)
+    n = G.size
     if what == WHAT_THETA:
         out = theta_values(seed, G)
     elif what == WHAT_THETA_LOCAL:

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star): indices / codes / records
+bit-exact; EF, scales, Delta and theta within 1e-6 relative (fp32) / 1e-2
+(bf16) — the kernels are written to the oracle's operation order, so the
+tests demand bitwise equality, which is stricter."""
+import numpy as np
+import pytest
+
+import oracle
+import slcgen
+from helpers import (bits, make_device_inputs, oracle_compress_shard, oracle_update_shard, seg_view)
+from slcgen import layouts
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2603_08163_b200 import slc  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _compress_gpu(plan, layout, seed, peer, dtype, special_period, warm, theta=None):
+    theta, tl, ef = make_device_inputs(plan, layout, seed, peer, dtype, special_period, warm, theta=theta)
+    rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
+    plan.compress(theta, tl, ef, rec)
+    return theta, tl, ef, rec
+
+
+@pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("special", [0, 4])
+def test_compress_parity(name, dtype, special):
+    layout = layouts.LAYOUTS[name]
+    plan = slc.Plan(layout, dtype=dtype)
+    warm = special == 0
+    theta, tl, ef, rec = _compress_gpu(plan, layout, 3, 1, dtype, special, warm)
+    assert plan.get_status() == slc.OK
+    ref_rec, ref_ef, _ = oracle_compress_shard(plan, layout, 3, 1, dtype, special, warm)
+    got = rec.cpu().numpy().view(np.uint32)
+    mism = np.nonzero(got != ref_rec)[0]
+    assert mism.size == 0, f"{mism.size} record words differ, first at word {mism[:5]}"
+    for s, e in zip(plan.segments, ref_ef):
+        g = seg_view(ef, s).cpu().numpy()
+        assert np.array_equal(bits(g), bits(e)), f"EF differs in segment {s.tensor}"
+
+
+@pytest.mark.parametrize("R", [1, 3, 8, 20])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_aggregate_update_parity(R, dtype):
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout, dtype=dtype)
+    recs, ref_recs = [], []
+    theta = None
+    for r in range(R):
+        theta, tl, ef, rec = _compress_gpu(plan, layout, 5, r, dtype, 8, True, theta=theta)
+        recs.append(rec)
+        rr, _, thetas = oracle_compress_shard(plan, layout, 5, r, dtype, 8, True)
+        assert np.array_equal(rec.cpu().numpy().view(np.uint32), rr)
+        ref_recs.append(rr)
+    alpha = 0.65
+    # unfused: decode_aggregate -> Delta, then update from Delta
+    agg = torch.zeros(plan.shard_elems, dtype=torch.float32, device=DEV)
+    plan.decode_aggregate(recs, agg)
+    ref_delta = oracle_update_shard(plan, thetas, ref_recs, alpha, only_delta=True)
+    for s, d in zip(plan.segments, ref_delta):
+        assert np.array_equal(bits(seg_view(agg, s).cpu().numpy()), bits(d))
+    th_unfused = theta.clone()
+    plan.outer_update(th_unfused, alpha, agg=agg)
+    # fused
+    th_fused = theta.clone()
+    plan.outer_update(th_fused, alpha, records=recs)
+    assert plan.get_status() == slc.OK
+    ref_theta = oracle_update_shard(plan, thetas, ref_recs, alpha)
+    for s, t in zip(plan.segments, ref_theta):
+        tb = bits(t)
+        fu = seg_view(th_fused, s).cpu()
+        un = seg_view(th_unfused, s).cpu()
+        if dtype == "bf16":
+            fu, un = fu.view(torch.int16), un.view(torch.int16)
+        assert np.array_equal(bits(fu.numpy()), tb)
+        assert np.array_equal(bits(un.numpy()), tb)
+
+
+def test_permutation_invariance_and_weights():
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout)
+    R = 12
+    recs, ref_recs, theta = [], [], None
+    for r in range(R):
+        theta, tl, ef, rec = _compress_gpu(plan, layout, 9, r, "f32", 0, True, theta=theta)
+        recs.append(rec)
+        rr, _, thetas = oracle_compress_shard(plan, layout, 9, r, "f32", 0, True)
+        ref_recs.append(rr)
+    rng = np.random.default_rng(0)
+    base = torch.zeros(plan.shard_elems, device=DEV)
+    plan.decode_aggregate(recs, base)
+    for _ in range(3):
+        perm = rng.permutation(R)
+        got = torch.zeros(plan.shard_elems, device=DEV)
+        plan.decode_aggregate([recs[i] for i in perm], got)
+        assert torch.equal(got.view(torch.int32), base.view(torch.int32))
+    # weighted (median-norm style weights), canonical peer-id order via headers
+    ids = [bytes(rng.integers(0, 256, 16, dtype=np.uint8)) for _ in range(R)]
+    w = rng.uniform(0.25, 2.0, R).astype(np.float32)
+    hdrs = [slc.make_header(plan, ids[r], base_round=7) for r in range(R)]
+    ref = oracle_update_shard(plan, thetas, ref_recs, 1.0, peer_ids=np.frombuffer(b"".join(ids), np.uint8),
+                              weights=w, only_delta=True)
+    for _ in range(3):
+        perm = rng.permutation(R)
+        got = torch.zeros(plan.shard_elems, device=DEV)
+        plan.decode_aggregate([recs[i] for i in perm], got, hdrs=[hdrs[i] for i in perm], weights=w[perm])
+        for s, d in zip(plan.segments, ref):
+            assert np.array_equal(bits(seg_view(got, s).cpu().numpy()), bits(d))
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+def test_sharding_invariance(nranks):
+    """Records of every shard concatenated in rank order == the 1-shard records;
+    EF identical (compression is independent per shard)."""
+    layout = layouts.LAYOUTS["ragged"] + [("w_big", (512, 256))]
+    full = slc.Plan(layout)
+    _, _, ef1, rec1 = _compress_gpu(full, layout, 11, 2, "f32", 4, True)
+    parts, first = [], 0
+    for g in range(nranks):
+        p = slc.Plan(layout, rank=g, nranks=nranks)
+        assert p.info.first_chunk == first
+        first += p.n_chunks
+        if p.n_chunks == 0:
+            continue
+        _, _, ef, rec = _compress_gpu(p, layout, 11, 2, "f32", 4, True)
+        parts.append(rec.cpu())
+        for s in p.segments:
+            ref = [t for t in full.segments if t.tensor == s.tensor][0]
+            lo = ref.shard_offset + s.tensor_begin - ref.tensor_begin
+            assert torch.equal(seg_view(ef, s).cpu().view(torch.int32),
+                               ef1[lo:lo + s.n_elems].cpu().view(torch.int32))
+    assert first == full.n_chunks
+    assert torch.equal(torch.cat(parts), rec1.cpu())
+
+
+@pytest.mark.parametrize("block,k", [(32, 16), (64, 16), (64, 32), (64, 128), (64, 256), (128, 256)])
+def test_geometry_sweep_parity(block, k):
+    g = slc.geometry(block=block, k=k)
+    og = oracle.geom(block=block, k=k)
+    B = block
+    layout = [("w", (2 * B, 3 * B)), ("v", (B * B * 2 + 77,)), ("r", (B + 3, B))]
+    plan = slc.Plan(layout, geom=g)
+    recs, ref_recs, theta = [], [], None
+    for r in range(3):
+        theta, tl, ef, rec = _compress_gpu(plan, layout, 13, r, "f32", 2, True, theta=theta)
+        rr, ref_ef, thetas = oracle_compress_shard(plan, layout, 13, r, "f32", 2, True, g=og)
+        assert np.array_equal(rec.cpu().numpy().view(np.uint32), rr)
+        for s, e in zip(plan.segments, ref_ef):
+            assert np.array_equal(bits(seg_view(ef, s).cpu().numpy()), bits(e))
+        recs.append(rec)
+        ref_recs.append(rr)
+    plan.outer_update(theta, 1.0, records=recs)
+    ref = oracle_update_shard(plan, thetas, ref_recs, 1.0, g=og)
+    for s, t in zip(plan.segments, ref):
+        assert np.array_equal(bits(seg_view(theta, s).cpu().numpy()), bits(t))
+
+
+def test_error_injection():
+    layout = [("w", (64, 128)), ("b", (4096,))]
+    plan = slc.Plan(layout)
+    theta, tl, ef = make_device_inputs(plan, layout, 1, 0)
+    rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
+    plan.compress(theta, tl, ef, rec)
+    assert plan.get_status() == slc.OK
+    for buf, val in [(theta, float("nan")), (tl, float("inf")), (ef, float("-inf"))]:
+        t2, l2, e2 = theta.clone(), tl.clone(), ef.clone()
+        {id(theta): t2, id(tl): l2, id(ef): e2}[id(buf)][100] = val
+        plan.compress(t2, l2, e2, rec)
+        assert plan.get_status() == slc.INVALID_DATA
+        assert plan.get_status() == slc.OK  # cleared
+    # fp16 scale overflow
+    t2 = theta.clone()
+    t2[:64] = 1e6
+    plan.compress(t2, tl, ef.clone(), rec)
+    assert plan.get_status() == slc.INVALID_DATA
+    # stale / mismatched headers
+    good = slc.make_header(plan, b"peer-a", base_round=3)
+    stale = slc.make_header(plan, b"peer-b", base_round=4)
+    agg = torch.zeros(plan.shard_elems, device=DEV)
+    with pytest.raises(slc.SlcError) as ei:
+        plan.decode_aggregate([rec, rec], agg, hdrs=[good, stale])
+    assert ei.value.status == slc.STALE
+    other = slc.Plan([("w", (64, 64)), ("b", (8192,))])
+    with pytest.raises(slc.SlcError) as ei:
+        plan.decode_aggregate([rec, rec], agg, hdrs=[good, slc.make_header(other, b"peer-b", 3)])
+    assert ei.value.status == slc.INVALID_ARGUMENT  # chunk range of another layout
+    dup = slc.make_header(plan, b"peer-a", base_round=3)
+    with pytest.raises(slc.SlcError) as ei:
+        plan.decode_aggregate([rec, rec], agg, hdrs=[good, dup])
+    assert ei.value.status == slc.INVALID_ARGUMENT
+    # misaligned dense buffer
+    big = torch.zeros(plan.shard_elems + 4, device=DEV)
+    with pytest.raises(slc.SlcError) as ei:
+        plan.compress(big[1:plan.shard_elems + 1], tl, ef, rec)
+    assert ei.value.status == slc.INVALID_ARGUMENT
+
+
+def test_generator_cuda_twin_bitwise():
+    rng = np.random.default_rng(1)
+    for what in [slcgen.WHAT_THETA, slcgen.WHAT_THETA_LOCAL, slcgen.WHAT_EF]:
+        for _ in range(3):
+            G0 = int(rng.integers(0, 2 ** 40))
+            n = 100003
+            ref = slcgen.generate(what, 42, 7, G0, n, special_period=3, warm_ef=True)
+            buf = torch.empty(n, dtype=torch.float32, device=DEV)
+            slcgen.fill_cuda(buf, what, 42, 7, G0, special_period=3, warm_ef=True)
+            assert np.array_equal(bits(buf.cpu().numpy()), bits(ref))
+    ref = slcgen.generate(slcgen.WHAT_THETA, 1, 0, 999, 5000, dtype="bf16")
+    buf = torch.empty(5000, dtype=torch.bfloat16, device=DEV)
+    slcgen.fill_cuda(buf, slcgen.WHAT_THETA, 1, 0, 999)
+    assert np.array_equal(buf.view(torch.int16).cpu().numpy().view(np.uint16), ref)
