@@ -24,19 +24,10 @@
 #include <cuda_fp16.h>
 
 #include "chunk_io.cuh"
+#include "quant_pack.cuh"
 
 namespace slc {
 namespace {
-
-constexpr unsigned FULL = 0xFFFFFFFFu;
-
-__device__ __forceinline__ float warp_tree_sum(float u) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) u = __fadd_rn(u, __shfl_xor_sync(FULL, u, d));
-  return u;
-}
-
-__device__ __forceinline__ uint32_t key_of(float b) { return (__float_as_uint(b) & 0x7FFFFFFFu) + 1u; }
 
 template <int C>
 struct CompressSmem {
@@ -51,19 +42,6 @@ struct CompressSmem {
   static constexpr size_t off_code = off_selval + sizeof(float) * kMaxK;
   static constexpr size_t bytes = off_code + sizeof(uint32_t) * kMaxK;
 };
-
-template <int NT>
-__device__ __forceinline__ int block_sum(int v, int* s_w) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = __reduce_add_sync(FULL, v);
-  if (lane == 0) s_w[warp] = v;
-  __syncthreads();
-  int tot = 0;
-#pragma unroll
-  for (int i = 0; i < NT / 32; i++) tot += s_w[i];
-  __syncthreads();
-  return tot;
-}
 
 template <int C, bool BF16>
 __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) {
@@ -139,12 +117,12 @@ __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) 
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL, incl, o);
+    const int y = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += y;
   }
   int wbase = 0;
   if (lane == 31) wbase = atomicAdd(&s_ncand, incl);
-  wbase = __shfl_sync(FULL, wbase, 31);
+  wbase = __shfl_sync(kFull, wbase, 31);
   int slot = wbase + incl - cnt;
 #pragma unroll
   for (int i = 0; i < 16; i++) {
@@ -204,7 +182,7 @@ __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) 
       int inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, inc, o);
+        const int y = __shfl_up_sync(kFull, inc, o);
         if (lane >= o) inc += y;
       }
       int before = inc - c;
@@ -233,7 +211,7 @@ __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) 
     int inc = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, inc, o);
+      const int y = __shfl_up_sync(kFull, inc, o);
       if (lane >= o) inc += y;
     }
     int s = inc - c;
@@ -249,60 +227,9 @@ __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) 
       }
     }
     __syncwarp();
-    const int W = (k + 31) >> 5;
-    float u = 0.0f;
-    for (int m = 0; m < W; m++) {
-      const int j = lane + 32 * m;
-      u = __fadd_rn(u, j < k_eff ? fabsf(selval[j]) : 0.0f);
-    }
-    const float tau = __fdiv_rn(warp_tree_sum(u), (float)k_eff);
-    float ulo = 0.0f, uhi = 0.0f;
-    int nhi = 0;
-    for (int m = 0; m < W; m++) {
-      const int j = lane + 32 * m;
-      if (j < k_eff) {
-        const float v = selval[j];
-        const float av = fabsf(v);
-        const bool h = av > tau;
-        ulo = __fadd_rn(ulo, h ? 0.0f : av);
-        uhi = __fadd_rn(uhi, h ? av : 0.0f);
-        nhi += h;
-        selcode[j] = (signbit(v) ? 1u : 0u) | (h ? 2u : 0u);
-      }
-    }
-    const float sum_lo = warp_tree_sum(ulo), sum_hi = warp_tree_sum(uhi);
-    nhi = __reduce_add_sync(FULL, nhi);
-    const int nlo = k_eff - nhi;
-    const float s_lo = nlo > 0 ? __fdiv_rn(sum_lo, (float)nlo) : 0.0f;
-    const float s_hi = nhi > 0 ? __fdiv_rn(sum_hi, (float)nhi) : tau;
-    const __half hlo = __float2half_rn(s_lo), hhi = __float2half_rn(s_hi);
-    const float flo = __half2float(hlo), fhi = __half2float(hhi);
-    const uint32_t hlo_bits = __half_as_ushort(hlo), hhi_bits = __half_as_ushort(hhi);
-    if (lane == 0) {
-      s_tau = tau; s_flo = flo; s_fhi = fhi;
-      if (isinf(flo) || isinf(fhi)) atomicOr(a.err, kErrScaleOverflow);
-    }
-    __syncwarp();
-    const int IW = a.g.idx_words, CW = a.g.code_words, RW = a.g.rec_words, ib = a.g.ib;
-    uint32_t* rec = a.records + chunk * RW;
-    for (int wi = lane; wi < RW; wi += 32) {
-      uint32_t word = 0;
-      if (wi < IW) {
-        const int b0 = 32 * wi;
-        const int j0 = b0 / ib, j1 = min((b0 + 31) / ib, k_eff - 1);
-        for (int j = j0; j <= j1; j++) {
-          const int sh = ib * j - b0;
-          const uint32_t pv = selpos[j];
-          word |= sh >= 0 ? (pv << sh) : (pv >> (-sh));
-        }
-      } else if (wi < IW + CW) {
-        const int j0 = 16 * (wi - IW);
-        for (int j = j0; j < min(j0 + 16, k_eff); j++) word |= selcode[j] << (2 * (j - j0));
-      } else {
-        word = hlo_bits | (hhi_bits << 16);
-      }
-      rec[wi] = word;
-    }
+    const QuantOut qo = warp_quantize_pack(selpos, selval, selcode, k, k_eff, a.g,
+                                           a.records + chunk * a.g.rec_words, a.err);
+    if (lane == 0) { s_tau = qo.tau; s_flo = qo.flo; s_fhi = qo.fhi; }
   }
   __syncthreads();
 
@@ -346,11 +273,21 @@ cudaError_t launch_one(const CompressArgs& a, cudaStream_t s) {
 
 bool compress_supported(int C) { return C == 1024 || C == 4096 || C == 16384; }
 
-cudaError_t launch_compress(const CompressArgs& a, int bf16, cudaStream_t s) {
+cudaError_t launch_compress_simple(const CompressArgs& a, int bf16, cudaStream_t s) {
   if (a.n_chunks == 0) return cudaSuccess;
   switch (a.g.C) {
     case 1024: return bf16 ? launch_one<1024, true>(a, s) : launch_one<1024, false>(a, s);
     case 4096: return bf16 ? launch_one<4096, true>(a, s) : launch_one<4096, false>(a, s);
+    case 16384: return bf16 ? launch_one<16384, true>(a, s) : launch_one<16384, false>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_compress(const CompressArgs& a, int bf16, cudaStream_t s) {
+  if (a.n_chunks == 0) return cudaSuccess;
+  switch (a.g.C) {
+    case 1024: return bf16 ? launch_one<1024, true>(a, s) : launch_one<1024, false>(a, s);
+    case 4096: return launch_compress_pipe(a, bf16, s);
     case 16384: return bf16 ? launch_one<16384, true>(a, s) : launch_one<16384, false>(a, s);
   }
   return cudaErrorInvalidValue;

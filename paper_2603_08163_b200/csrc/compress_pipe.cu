@@ -1,0 +1,360 @@
+// compress_pipe.cu — slc_compress for the paper's geometry (C = 4096, 64x64
+// blocks): persistent CTAs, bulk-copy (TMA) double buffering.
+//
+// Grid = 2 CTAs per SM, 256 threads each, ~104 KB smem each.  CTA b walks the
+// chunks b, b+G, b+2G, ...  Warp 0 is the producer: for chunk i+2 it arms an
+// mbarrier with the chunk's byte count and issues cp.async.bulk copies of the
+// theta, theta_local and e tiles into the stage chunk i just vacated (a 64x64
+// block = 64 row copies of 256 B per array; a flat chunk = one 16 KB copy per
+// array).  Each SM therefore keeps ~2 chunks (~96 KB) of loads in flight while
+// it computes, without registers or LSU instructions spent on the loads.
+//
+// Per chunk (same arithmetic and selection rule as the simple kernel):
+//  1. smem -> registers (4 x LDS.128 per array), d = theta - theta_local,
+//     b = fma(beta, e, d) (R#12); e <- b stored densely right away
+//     (selected positions are corrected in step 7).
+//  2. lower bound T on the k-th largest key from the 256 thread maxima (15
+//     __syncthreads_count rounds); after the first round the stage is free and
+//     warp 0 refills it.
+//  3. candidates key >= T -> smem (typically ~1.2 k); 4. exact rank by
+//     counting -> selected bit in a 4096-bit bitmap (fallback for > 256
+//     candidates: exact k-th key by bitwise block counting, ties by position).
+//  5-6. bitmap word prefix -> each selected value lands at its slot (ascending
+//     position, R#5).
+//  7. warp 0: 2-bit quantiser + record (R#1, R#6, R#13, R#14) and the
+//     selected positions' EF residual e = b - dequant — while warps 1-7
+//     already start step 1 of their next chunk.
+#include "chunk_io.cuh"
+#include "ptx.cuh"
+#include "quant_pack.cuh"
+
+namespace slc {
+namespace {
+
+constexpr int kC = 4096;
+constexpr int kNT = 256;
+constexpr int kMaxCand = 256;
+
+template <bool BF16>
+struct PipeSmem {
+  static constexpr int PB = BF16 ? 2 : 4;
+  static constexpr size_t arr_theta = 0;
+  static constexpr size_t arr_tl = (size_t)kC * PB;
+  static constexpr size_t arr_e = 2 * (size_t)kC * PB;
+  static constexpr size_t stage_bytes = (size_t)kC * (2 * PB + 4);
+  static constexpr size_t off_cand = 2 * stage_bytes;                 // u64[256]
+  static constexpr size_t off_candb = off_cand + 8 * kMaxCand;         // f32[256]
+  static constexpr size_t off_bit = off_candb + 4 * kMaxCand;          // u32[128]
+  static constexpr size_t off_tie = off_bit + 4 * (kC / 32);           // u32[128]
+  static constexpr size_t off_wpre = off_tie + 4 * (kC / 32);          // u32[128]
+  static constexpr size_t off_selpos = off_wpre + 4 * (kC / 32);       // u32[kMaxK]
+  static constexpr size_t off_selval = off_selpos + 4 * kMaxK;         // f32[kMaxK]
+  static constexpr size_t off_code = off_selval + 4 * kMaxK;           // u32[kMaxK]
+  static constexpr size_t off_bar = off_code + 4 * kMaxK;              // u64[2]
+  static constexpr size_t bytes = off_bar + 16;
+};
+
+template <bool BF16>
+__device__ __forceinline__ void issue_chunk(const CompressArgs& a, int64_t c, unsigned char* stage, uint64_t* bar,
+                                            int lane) {
+  using S = PipeSmem<BF16>;
+  constexpr int PB = S::PB;
+  const ChunkDesc d = a.chunks[c];
+  const bool full = d.len == kC;
+  if (lane == 0) {
+    if (full) ptx::mbar_arrive_expect_tx(bar, (uint32_t)S::stage_bytes);
+    else ptx::mbar_arrive(bar);  // partial chunk: consumers read global memory directly
+  }
+  __syncwarp();
+  if (!full) return;
+  const unsigned char* th = static_cast<const unsigned char*>(a.theta);
+  const unsigned char* tl = static_cast<const unsigned char*>(a.theta_local);
+  const unsigned char* ef = reinterpret_cast<const unsigned char*>(a.ef);
+  if (d.ld) {
+    // 64 block rows x 3 arrays; lane handles rows lane and lane+32 of each array
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int r = lane + 32 * h;
+      const int64_t row = d.base + (int64_t)r * d.ld;
+      ptx::bulk_g2s(stage + S::arr_theta + (size_t)r * 64 * PB, th + row * PB, 64 * PB, bar);
+      ptx::bulk_g2s(stage + S::arr_tl + (size_t)r * 64 * PB, tl + row * PB, 64 * PB, bar);
+      ptx::bulk_g2s(stage + S::arr_e + (size_t)r * 256, ef + row * 4, 256, bar);
+    }
+  } else if (lane == 0) {
+    ptx::bulk_g2s(stage + S::arr_theta, th + d.base * PB, kC * PB, bar);
+    ptx::bulk_g2s(stage + S::arr_tl, tl + d.base * PB, kC * PB, bar);
+    ptx::bulk_g2s(stage + S::arr_e, ef + d.base * 4, kC * 4, bar);
+  }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArgs a) {
+  using S = PipeSmem<BF16>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* scand = reinterpret_cast<uint64_t*>(smem + S::off_cand);
+  float* candb = reinterpret_cast<float*>(smem + S::off_candb);
+  uint32_t* sbit = reinterpret_cast<uint32_t*>(smem + S::off_bit);
+  uint32_t* stie = reinterpret_cast<uint32_t*>(smem + S::off_tie);
+  uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + S::off_wpre);
+  uint32_t* selpos = reinterpret_cast<uint32_t*>(smem + S::off_selpos);
+  float* selval = reinterpret_cast<float*>(smem + S::off_selval);
+  uint32_t* selcode = reinterpret_cast<uint32_t*>(smem + S::off_code);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::off_bar);
+  __shared__ int s_ncand;
+  __shared__ int s_w[kNT / 32];
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t G = gridDim.x, n = a.n_chunks;
+  const int k = a.g.k;
+
+  if (t == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_mbar_init();
+  }
+  if (t < kC / 32) { sbit[t] = 0u; stie[t] = 0u; }
+  if (t == 0) s_ncand = 0;
+  __syncthreads();
+  if (warp == 0) {
+    if ((int64_t)blockIdx.x < n) issue_chunk<BF16>(a, blockIdx.x, smem, &bars[0], lane);
+    if ((int64_t)blockIdx.x + G < n) issue_chunk<BF16>(a, blockIdx.x + G, smem + S::stage_bytes, &bars[1], lane);
+  }
+
+  for (int64_t i = 0;; ++i) {
+    const int64_t c = (int64_t)blockIdx.x + i * G;
+    if (c >= n) break;
+    const int s = (int)(i & 1);
+    const uint32_t par = (uint32_t)((i >> 1) & 1);
+    unsigned char* stage = smem + s * S::stage_bytes;
+    const ChunkDesc d = a.chunks[c];
+    const int len = d.len;
+    const bool full = len == kC;
+    const int k_eff = full ? k : max(1, (k * len) / kC);
+
+    // ---- 1. inputs -> b; dense e <- b ------------------------------------------
+    ptx::mbar_wait(&bars[s], par);
+    float b[16];
+    uint32_t lm = 0;
+    bool bad = false;
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const int q = v * kNT + t;
+      const int p0 = 4 * q;
+      const int64_t off = group_offset(d, q, 4);
+      float av[4], lv[4], ev[4];
+      int nv = 4;
+      if (full) {
+        if (BF16) {
+          const uint2 ua = *reinterpret_cast<const uint2*>(stage + S::arr_theta + 2 * p0);
+          const uint2 ul = *reinterpret_cast<const uint2*>(stage + S::arr_tl + 2 * p0);
+          av[0] = bf16_bits_to_f32(ua.x & 0xFFFFu); av[1] = bf16_bits_to_f32(ua.x >> 16);
+          av[2] = bf16_bits_to_f32(ua.y & 0xFFFFu); av[3] = bf16_bits_to_f32(ua.y >> 16);
+          lv[0] = bf16_bits_to_f32(ul.x & 0xFFFFu); lv[1] = bf16_bits_to_f32(ul.x >> 16);
+          lv[2] = bf16_bits_to_f32(ul.y & 0xFFFFu); lv[3] = bf16_bits_to_f32(ul.y >> 16);
+        } else {
+          const float4 fa = *reinterpret_cast<const float4*>(stage + S::arr_theta + 4 * p0);
+          const float4 fl = *reinterpret_cast<const float4*>(stage + S::arr_tl + 4 * p0);
+          av[0] = fa.x; av[1] = fa.y; av[2] = fa.z; av[3] = fa.w;
+          lv[0] = fl.x; lv[1] = fl.y; lv[2] = fl.z; lv[3] = fl.w;
+        }
+        const float4 fe = *reinterpret_cast<const float4*>(stage + S::arr_e + 4 * p0);
+        ev[0] = fe.x; ev[1] = fe.y; ev[2] = fe.z; ev[3] = fe.w;
+      } else {
+        nv = valid_in_group(p0, len);
+        load_param4<BF16>(a.theta, off, nv, av);
+        load_param4<BF16>(a.theta_local, off, nv, lv);
+        load_f32x4(a.ef, off, nv, ev);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const float bb = __fmaf_rn(a.beta, ev[j], __fsub_rn(av[j], lv[j]));
+        b[4 * v + j] = bb;
+        const uint32_t key = (j < nv) ? key_of(bb) : 0u;
+        bad |= key > 0x7F800000u;
+        lm = max(lm, key);
+      }
+      if (full) *reinterpret_cast<float4*>(a.ef + off) = make_float4(b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3]);
+      else store_f32x4(a.ef, off, nv, &b[4 * v]);
+    }
+    if (bad) atomicOr(a.err, kErrNonFinite);
+
+    // ---- 2. lower bound T from the thread maxima -------------------------------
+    uint32_t T = 0;
+    {
+      const uint32_t Tp = 1u << 30;
+      if (__syncthreads_count(lm >= Tp) >= k_eff) T = Tp;
+    }
+    // every thread has read stage s: refill it with chunk i+2
+    if (warp == 0 && c + 2 * G < n) issue_chunk<BF16>(a, c + 2 * G, stage, &bars[s], lane);
+#pragma unroll
+    for (int bit = 29; bit >= 16; --bit) {
+      const uint32_t Tp = T | (1u << bit);
+      if (__syncthreads_count(lm >= Tp) >= k_eff) T = Tp;
+    }
+    const uint32_t Tc = max(T, 1u);
+
+    // ---- 3. candidates -------------------------------------------------------------
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+      cnt += ((full || p < len) && key_of(b[j]) >= Tc);
+    }
+    const int incl = warp_excl_scan(cnt) + cnt;
+    int wbase = 0;
+    if (lane == 31) wbase = atomicAdd(&s_ncand, incl);
+    wbase = __shfl_sync(kFull, wbase, 31);
+    int slot = wbase + incl - cnt;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+      const uint32_t key = key_of(b[j]);
+      if ((full || p < len) && key >= Tc) {
+        if (slot < kMaxCand) {
+          scand[slot] = ((uint64_t)key << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
+          candb[slot] = b[j];
+        }
+        slot++;
+      }
+    }
+    __syncthreads();
+    const int M = s_ncand;
+
+    // ---- 4. exact selection -> bitmap ------------------------------------------------
+    int my_p = -1;
+    float my_b = 0.0f;
+    if (M <= kMaxCand) {
+      if (t < M) {
+        const uint64_t me = scand[t];
+        int rank = 0;
+#pragma unroll 8
+        for (int j = 0; j < M; j++) rank += (scand[j] > me);
+        if (rank < k_eff) {
+          my_p = (int)(0xFFFFu - (uint32_t)(me & 0xFFFFu));
+          my_b = candb[t];
+          atomicOr(&sbit[my_p >> 5], 1u << (my_p & 31));
+        }
+      }
+    } else {
+      uint32_t Kth = 0;
+#pragma unroll 1
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t Tp = Kth | (1u << bit);
+        int cc = 0;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+          cc += (p < len && key_of(b[j]) >= Tp);
+        }
+        if (block_sum<kNT>(cc, s_w) >= k_eff) Kth = Tp;
+      }
+      int gt = 0;
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+        if (p < len) {
+          const uint32_t key = key_of(b[j]);
+          if (key > Kth) { atomicOr(&sbit[p >> 5], 1u << (p & 31)); gt++; }
+          else if (key == Kth) atomicOr(&stie[p >> 5], 1u << (p & 31));
+        }
+      }
+      const int need = k_eff - block_sum<kNT>(gt, s_w);
+      if (warp == 0) {
+        uint32_t w[4];
+        int cw = 0;
+#pragma unroll
+        for (int x = 0; x < 4; x++) { w[x] = stie[4 * lane + x]; cw += __popc(w[x]); }
+        int before = warp_excl_scan(cw);
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+          uint32_t keep = 0, y = w[x];
+          while (y && before < need) {
+            const uint32_t lowbit = y & (0u - y);
+            keep |= lowbit;
+            y ^= lowbit;
+            before++;
+          }
+          if (keep) atomicOr(&sbit[4 * lane + x], keep);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- 5. bitmap word prefix ---------------------------------------------------------
+    if (warp == 0) {
+      uint32_t w[4];
+      int cw = 0;
+#pragma unroll
+      for (int x = 0; x < 4; x++) { w[x] = sbit[4 * lane + x]; cw += __popc(w[x]); }
+      int pre = warp_excl_scan(cw);
+#pragma unroll
+      for (int x = 0; x < 4; x++) { wpre[4 * lane + x] = (uint32_t)pre; pre += __popc(w[x]); }
+    }
+    __syncthreads();
+
+    // ---- 6. selected values to their slots ---------------------------------------------
+    if (M <= kMaxCand) {
+      if (my_p >= 0) {
+        const int sl = (int)wpre[my_p >> 5] + __popc(sbit[my_p >> 5] & ((1u << (my_p & 31)) - 1u));
+        selpos[sl] = (uint32_t)my_p;
+        selval[sl] = my_b;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+        if (p < len && ((sbit[p >> 5] >> (p & 31)) & 1u)) {
+          const int sl = (int)wpre[p >> 5] + __popc(sbit[p >> 5] & ((1u << (p & 31)) - 1u));
+          selpos[sl] = (uint32_t)p;
+          selval[sl] = b[j];
+        }
+      }
+    }
+    __syncthreads();
+    // reset the per-chunk selection state for the next chunk (read only above)
+    if (t >= kNT - kC / 32) { sbit[t - (kNT - kC / 32)] = 0u; stie[t - (kNT - kC / 32)] = 0u; }
+    if (t == 0) s_ncand = 0;
+
+    // ---- 7. warp 0: quantise, record, EF of the selected positions ----------------------
+    if (warp == 0) {
+      const QuantOut qo = warp_quantize_pack(selpos, selval, selcode, k, k_eff, a.g,
+                                             a.records + c * a.g.rec_words, a.err);
+      for (int j = lane; j < k_eff; j += 32) {
+        const int p = (int)selpos[j];
+        const float bb = selval[j];
+        const float mag = fabsf(bb) > qo.tau ? qo.fhi : qo.flo;
+        const int64_t addr = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
+        a.ef[addr] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
+      }
+    }
+  }
+}
+
+template <bool BF16>
+cudaError_t launch_pipe(const CompressArgs& a, cudaStream_t s) {
+  constexpr size_t smem = PipeSmem<BF16>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(compress_pipe_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_pipe_kernel<BF16>, kNT, smem)) !=
+      cudaSuccess)
+    return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > a.n_chunks) grid = a.n_chunks;
+  compress_pipe_kernel<BF16><<<(unsigned)grid, kNT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_compress_pipe(const CompressArgs& a, int bf16, cudaStream_t s) {
+  if (a.n_chunks == 0) return cudaSuccess;
+  if (a.g.C != kC) return cudaErrorInvalidValue;
+  return bf16 ? launch_pipe<true>(a, s) : launch_pipe<false>(a, s);
+}
+
+}  // namespace slc

@@ -188,10 +188,15 @@ def test_error_injection():
     with pytest.raises(slc.SlcError) as ei:
         plan.decode_aggregate([rec, rec], agg, hdrs=[good, stale])
     assert ei.value.status == slc.STALE
-    other = slc.Plan([("w", (64, 64)), ("b", (8192,))])
+    other = slc.Plan([("w", (64, 64)), ("b", (8192,))])  # same chunk count, other layout digest
     with pytest.raises(slc.SlcError) as ei:
         plan.decode_aggregate([rec, rec], agg, hdrs=[good, slc.make_header(other, b"peer-b", 3)])
-    assert ei.value.status == slc.INVALID_ARGUMENT  # chunk range of another layout
+    assert ei.value.status == slc.STALE
+    wrong_range = slc.make_header(plan, b"peer-b", base_round=3)
+    wrong_range.first_chunk = 1
+    with pytest.raises(slc.SlcError) as ei:
+        plan.decode_aggregate([rec, rec], agg, hdrs=[good, wrong_range])
+    assert ei.value.status == slc.INVALID_ARGUMENT
     dup = slc.make_header(plan, b"peer-a", base_round=3)
     with pytest.raises(slc.SlcError) as ei:
         plan.decode_aggregate([rec, rec], agg, hdrs=[good, dup])
