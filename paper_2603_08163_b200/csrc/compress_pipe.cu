@@ -1,29 +1,29 @@
 // compress_pipe.cu — slc_compress for the paper's geometry (C = 4096, 64x64
-// blocks): persistent CTAs, bulk-copy (TMA) double buffering.
+// blocks): persistent, warp-specialised, cp.async double-buffered.
 //
-// Grid = 2 CTAs per SM, 256 threads each, ~104 KB smem each.  CTA b walks the
-// chunks b, b+G, b+2G, ...  Warp 0 is the producer: for chunk i+2 it arms an
-// mbarrier with the chunk's byte count and issues cp.async.bulk copies of the
-// theta, theta_local and e tiles into the stage chunk i just vacated (a 64x64
-// block = 64 row copies of 256 B per array; a flat chunk = one 16 KB copy per
-// array).  Each SM therefore keeps ~2 chunks (~96 KB) of loads in flight while
-// it computes, without registers or LSU instructions spent on the loads.
+// CTA = 8 compute warps + 1 quantiser warp; 2 CTAs per SM (~106 KB smem each).
+// CTA b walks chunks b, b+G, b+2G, ...
 //
-// Per chunk (same arithmetic and selection rule as the simple kernel):
-//  1. smem -> registers (4 x LDS.128 per array), d = theta - theta_local,
-//     b = fma(beta, e, d) (R#12); e <- b stored densely right away
-//     (selected positions are corrected in step 7).
-//  2. lower bound T on the k-th largest key from the 256 thread maxima (15
-//     __syncthreads_count rounds); after the first round the stage is free and
-//     warp 0 refills it.
-//  3. candidates key >= T -> smem (typically ~1.2 k); 4. exact rank by
-//     counting -> selected bit in a 4096-bit bitmap (fallback for > 256
-//     candidates: exact k-th key by bitwise block counting, ties by position).
-//  5-6. bitmap word prefix -> each selected value lands at its slot (ascending
-//     position, R#5).
-//  7. warp 0: 2-bit quantiser + record (R#1, R#6, R#13, R#14) and the
-//     selected positions' EF residual e = b - dequant — while warps 1-7
-//     already start step 1 of their next chunk.
+//  compute warps, chunk i (stage s = i & 1):
+//   1. wait the stage's mbarrier; smem -> registers (LDS.128), d = theta -
+//      theta_local, b = fma(beta, e, d) (R#12); e <- b stored densely
+//      at once (selected positions are corrected by the quantiser warp);
+//   2. lower bound T on the k-th largest key: the largest T with at least k of
+//      the 256 thread maxima >= T (bits 30..16, one barrier.red.popc each).  After
+//      the first round every thread is done with stage s, so each thread
+//      issues its 12 x 16-byte cp.async of chunk i+2 into it and arrives on the
+//      stage mbarrier with cp.async.mbarrier.arrive.noinc — loads are spread
+//      over all 256 threads, ~96 KB in flight per SM, no registers held;
+//   3. candidates key >= T (typically ~1.2 k) -> smem as key<<16 | ~pos;
+//   4. exact rank by counting -> 4096-bit selection bitmap (fallback when more
+//      than 256 candidates: exact k-th key by bitwise block counting, ties to
+//      the lower position);
+//   5. bitmap word prefix; 6. each selected value lands at its slot (ascending
+//      position) in hand-off buffer i & 1 -> named-barrier arrive.
+//  quantiser warp, chunk i: named-barrier sync on the hand-off buffer; 2-bit
+//   quantiser + record (R#1, R#6, R#13, R#14); EF of the selected positions
+//   e = b - dequant; release the buffer.  It runs concurrently with the
+//   compute warps' next chunk, so its serial latency is off the critical path.
 #include "chunk_io.cuh"
 #include "ptx.cuh"
 #include "quant_pack.cuh"
@@ -32,8 +32,10 @@ namespace slc {
 namespace {
 
 constexpr int kC = 4096;
-constexpr int kNT = 256;
+constexpr int kNT = 256;                // compute threads
+constexpr int kThreads = kNT + 32;      // + quantiser warp
 constexpr int kMaxCand = 256;
+enum : int { kBarCompute = 1, kBarReady0 = 2, kBarFree0 = 4 };
 
 template <bool BF16>
 struct PipeSmem {
@@ -47,48 +49,45 @@ struct PipeSmem {
   static constexpr size_t off_bit = off_candb + 4 * kMaxCand;          // u32[128]
   static constexpr size_t off_tie = off_bit + 4 * (kC / 32);           // u32[128]
   static constexpr size_t off_wpre = off_tie + 4 * (kC / 32);          // u32[128]
-  static constexpr size_t off_selpos = off_wpre + 4 * (kC / 32);       // u32[kMaxK]
-  static constexpr size_t off_selval = off_selpos + 4 * kMaxK;         // f32[kMaxK]
-  static constexpr size_t off_code = off_selval + 4 * kMaxK;           // u32[kMaxK]
+  static constexpr size_t off_selpos = off_wpre + 4 * (kC / 32);       // u32[2][kMaxK]
+  static constexpr size_t off_selval = off_selpos + 8 * kMaxK;         // f32[2][kMaxK]
+  static constexpr size_t off_code = off_selval + 8 * kMaxK;           // u32[kMaxK]
   static constexpr size_t off_bar = off_code + 4 * kMaxK;              // u64[2]
   static constexpr size_t bytes = off_bar + 16;
 };
 
+// all 256 compute threads: cp.async chunk c into `stage`, then arrive on `bar`
 template <bool BF16>
-__device__ __forceinline__ void issue_chunk(const CompressArgs& a, int64_t c, unsigned char* stage, uint64_t* bar,
-                                            int lane) {
+__device__ __forceinline__ void prefetch_chunk(const CompressArgs& a, int64_t c, unsigned char* stage, uint64_t* bar,
+                                               int t) {
   using S = PipeSmem<BF16>;
   constexpr int PB = S::PB;
   const ChunkDesc d = a.chunks[c];
-  const bool full = d.len == kC;
-  if (lane == 0) {
-    if (full) ptx::mbar_arrive_expect_tx(bar, (uint32_t)S::stage_bytes);
-    else ptx::mbar_arrive(bar);  // partial chunk: consumers read global memory directly
-  }
-  __syncwarp();
-  if (!full) return;
-  const unsigned char* th = static_cast<const unsigned char*>(a.theta);
-  const unsigned char* tl = static_cast<const unsigned char*>(a.theta_local);
-  const unsigned char* ef = reinterpret_cast<const unsigned char*>(a.ef);
-  if (d.ld) {
-    // 64 block rows x 3 arrays; lane handles rows lane and lane+32 of each array
+  if (d.len == kC) {
+    const unsigned char* th = static_cast<const unsigned char*>(a.theta);
+    const unsigned char* tl = static_cast<const unsigned char*>(a.theta_local);
+    const unsigned char* ef = reinterpret_cast<const unsigned char*>(a.ef);
+    constexpr int EPP = 16 / PB;       // elements per 16-byte piece
+    constexpr int PP = kC / EPP;       // pieces per param array
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int r = lane + 32 * h;
-      const int64_t row = d.base + (int64_t)r * d.ld;
-      ptx::bulk_g2s(stage + S::arr_theta + (size_t)r * 64 * PB, th + row * PB, 64 * PB, bar);
-      ptx::bulk_g2s(stage + S::arr_tl + (size_t)r * 64 * PB, tl + row * PB, 64 * PB, bar);
-      ptx::bulk_g2s(stage + S::arr_e + (size_t)r * 256, ef + row * 4, 256, bar);
+    for (int m = t; m < PP; m += kNT) {
+      const int p = m * EPP;
+      const int64_t g = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
+      ptx::cp_async16(stage + S::arr_theta + (size_t)p * PB, th + g * PB);
+      ptx::cp_async16(stage + S::arr_tl + (size_t)p * PB, tl + g * PB);
     }
-  } else if (lane == 0) {
-    ptx::bulk_g2s(stage + S::arr_theta, th + d.base * PB, kC * PB, bar);
-    ptx::bulk_g2s(stage + S::arr_tl, tl + d.base * PB, kC * PB, bar);
-    ptx::bulk_g2s(stage + S::arr_e, ef + d.base * 4, kC * 4, bar);
+#pragma unroll
+    for (int m = t; m < kC / 4; m += kNT) {
+      const int p = 4 * m;
+      const int64_t g = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
+      ptx::cp_async16(stage + S::arr_e + (size_t)p * 4, ef + g * 4);
+    }
   }
+  ptx::cp_async_arrive_noinc(bar);  // partial chunk: consumers read global memory directly
 }
 
-template <bool BF16>
-__global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArgs a) {
+template <bool BF16, int KC, int IBC>
+__global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const CompressArgs a) {
   using S = PipeSmem<BF16>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* scand = reinterpret_cast<uint64_t*>(smem + S::off_cand);
@@ -105,20 +104,52 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t G = gridDim.x, n = a.n_chunks;
-  const int k = a.g.k;
+  const int k = KC ? KC : a.g.k;
 
   if (t == 0) {
-    ptx::mbar_init(&bars[0], 1);
-    ptx::mbar_init(&bars[1], 1);
+    ptx::mbar_init(&bars[0], kNT);
+    ptx::mbar_init(&bars[1], kNT);
     ptx::fence_mbar_init();
   }
   if (t < kC / 32) { sbit[t] = 0u; stie[t] = 0u; }
   if (t == 0) s_ncand = 0;
   __syncthreads();
-  if (warp == 0) {
-    if ((int64_t)blockIdx.x < n) issue_chunk<BF16>(a, blockIdx.x, smem, &bars[0], lane);
-    if ((int64_t)blockIdx.x + G < n) issue_chunk<BF16>(a, blockIdx.x + G, smem + S::stage_bytes, &bars[1], lane);
+
+  if (warp == kNT / 32) {
+    // ======================= quantiser warp =======================
+    ptx::named_arrive<kBarFree0>(kThreads);
+    ptx::named_arrive<kBarFree0 + 1>(kThreads);
+    for (int64_t i = 0;; ++i) {
+      const int64_t c = (int64_t)blockIdx.x + i * G;
+      if (c >= n) break;
+      const int buf = (int)(i & 1);
+      const ChunkDesc d = a.chunks[c];
+      const int k_eff = d.len == kC ? k : max(1, (k * d.len) / kC);
+      if (buf) ptx::named_sync<kBarReady0 + 1>(kThreads);
+      else ptx::named_sync<kBarReady0>(kThreads);
+      const uint32_t* sp = selpos + buf * kMaxK;
+      const float* sv = selval + buf * kMaxK;
+      const QuantOut qo =
+          warp_quantize_pack<KC, IBC>(sp, sv, selcode, k, k_eff, a.g, a.records + c * a.g.rec_words, a.err);
+      for (int j = lane; j < k_eff; j += 32) {
+        const int p = (int)sp[j];
+        const float bb = sv[j];
+        const float mag = fabsf(bb) > qo.tau ? qo.fhi : qo.flo;
+        const int64_t addr = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
+        a.ef[addr] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
+      }
+      __syncwarp();
+      if (c + 2 * G < n) {
+        if (buf) ptx::named_arrive<kBarFree0 + 1>(kThreads);
+        else ptx::named_arrive<kBarFree0>(kThreads);
+      }
+    }
+    return;
   }
+
+  // ======================= compute warps =======================
+  if ((int64_t)blockIdx.x < n) prefetch_chunk<BF16>(a, blockIdx.x, smem, &bars[0], t);
+  if ((int64_t)blockIdx.x + G < n) prefetch_chunk<BF16>(a, blockIdx.x + G, smem + S::stage_bytes, &bars[1], t);
 
   for (int64_t i = 0;; ++i) {
     const int64_t c = (int64_t)blockIdx.x + i * G;
@@ -131,7 +162,7 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
     const bool full = len == kC;
     const int k_eff = full ? k : max(1, (k * len) / kC);
 
-    // ---- 1. inputs -> b; dense e <- b ------------------------------------------
+    // ---- 1. inputs -> b; dense e <- b -------------------------------------------
     ptx::mbar_wait(&bars[s], par);
     float b[16];
     uint32_t lm = 0;
@@ -178,22 +209,20 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
     }
     if (bad) atomicOr(a.err, kErrNonFinite);
 
-    // ---- 2. lower bound T from the thread maxima -------------------------------
+    // ---- 2. lower bound T from the thread maxima; refill the stage ---------------
     uint32_t T = 0;
-    {
-      const uint32_t Tp = 1u << 30;
-      if (__syncthreads_count(lm >= Tp) >= k_eff) T = Tp;
-    }
-    // every thread has read stage s: refill it with chunk i+2
-    if (warp == 0 && c + 2 * G < n) issue_chunk<BF16>(a, c + 2 * G, stage, &bars[s], lane);
+    if (ptx::named_count<kBarCompute>(kNT, lm >= (1u << 30)) >= k_eff) T = 1u << 30;
+    if (c + 2 * G < n) prefetch_chunk<BF16>(a, c + 2 * G, stage, &bars[s], t);
+    if (t >= kNT - kC / 32) { sbit[t - (kNT - kC / 32)] = 0u; stie[t - (kNT - kC / 32)] = 0u; }
+    if (t == 0) s_ncand = 0;
 #pragma unroll
     for (int bit = 29; bit >= 16; --bit) {
       const uint32_t Tp = T | (1u << bit);
-      if (__syncthreads_count(lm >= Tp) >= k_eff) T = Tp;
+      if (ptx::named_count<kBarCompute>(kNT, lm >= Tp) >= k_eff) T = Tp;
     }
     const uint32_t Tc = max(T, 1u);
 
-    // ---- 3. candidates -------------------------------------------------------------
+    // ---- 3. candidates -----------------------------------------------------------------
     int cnt = 0;
 #pragma unroll
     for (int j = 0; j < 16; j++) {
@@ -217,10 +246,10 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
         slot++;
       }
     }
-    __syncthreads();
+    ptx::named_sync<kBarCompute>(kNT);
     const int M = s_ncand;
 
-    // ---- 4. exact selection -> bitmap ------------------------------------------------
+    // ---- 4. exact selection -> bitmap --------------------------------------------------
     int my_p = -1;
     float my_b = 0.0f;
     if (M <= kMaxCand) {
@@ -246,7 +275,7 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
           const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
           cc += (p < len && key_of(b[j]) >= Tp);
         }
-        if (block_sum<kNT>(cc, s_w) >= k_eff) Kth = Tp;
+        if (block_sum_named<kNT, kBarCompute>(cc, s_w) >= k_eff) Kth = Tp;
       }
       int gt = 0;
 #pragma unroll
@@ -258,7 +287,7 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
           else if (key == Kth) atomicOr(&stie[p >> 5], 1u << (p & 31));
         }
       }
-      const int need = k_eff - block_sum<kNT>(gt, s_w);
+      const int need = k_eff - block_sum_named<kNT, kBarCompute>(gt, s_w);
       if (warp == 0) {
         uint32_t w[4];
         int cw = 0;
@@ -278,9 +307,9 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
         }
       }
     }
-    __syncthreads();
+    ptx::named_sync<kBarCompute>(kNT);
 
-    // ---- 5. bitmap word prefix ---------------------------------------------------------
+    // ---- 5. bitmap word prefix -----------------------------------------------------------
     if (warp == 0) {
       uint32_t w[4];
       int cw = 0;
@@ -290,14 +319,20 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
 #pragma unroll
       for (int x = 0; x < 4; x++) { wpre[4 * lane + x] = (uint32_t)pre; pre += __popc(w[x]); }
     }
-    __syncthreads();
+    // hand-off buffer i & 1 must have been released by the quantiser (chunk i-2)
+    const int buf = (int)(i & 1);
+    if (buf) ptx::named_sync<kBarFree0 + 1>(kThreads);
+    else ptx::named_sync<kBarFree0>(kThreads);
+    ptx::named_sync<kBarCompute>(kNT);
 
-    // ---- 6. selected values to their slots ---------------------------------------------
+    // ---- 6. selected values to their slots, hand off --------------------------------------
+    uint32_t* sp = selpos + buf * kMaxK;
+    float* sv = selval + buf * kMaxK;
     if (M <= kMaxCand) {
       if (my_p >= 0) {
         const int sl = (int)wpre[my_p >> 5] + __popc(sbit[my_p >> 5] & ((1u << (my_p & 31)) - 1u));
-        selpos[sl] = (uint32_t)my_p;
-        selval[sl] = my_b;
+        sp[sl] = (uint32_t)my_p;
+        sv[sl] = my_b;
       }
     } else {
 #pragma unroll
@@ -305,48 +340,38 @@ __global__ void __launch_bounds__(kNT, 2) compress_pipe_kernel(const CompressArg
         const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
         if (p < len && ((sbit[p >> 5] >> (p & 31)) & 1u)) {
           const int sl = (int)wpre[p >> 5] + __popc(sbit[p >> 5] & ((1u << (p & 31)) - 1u));
-          selpos[sl] = (uint32_t)p;
-          selval[sl] = b[j];
+          sp[sl] = (uint32_t)p;
+          sv[sl] = b[j];
         }
       }
     }
-    __syncthreads();
-    // reset the per-chunk selection state for the next chunk (read only above)
-    if (t >= kNT - kC / 32) { sbit[t - (kNT - kC / 32)] = 0u; stie[t - (kNT - kC / 32)] = 0u; }
-    if (t == 0) s_ncand = 0;
-
-    // ---- 7. warp 0: quantise, record, EF of the selected positions ----------------------
-    if (warp == 0) {
-      const QuantOut qo = warp_quantize_pack(selpos, selval, selcode, k, k_eff, a.g,
-                                             a.records + c * a.g.rec_words, a.err);
-      for (int j = lane; j < k_eff; j += 32) {
-        const int p = (int)selpos[j];
-        const float bb = selval[j];
-        const float mag = fabsf(bb) > qo.tau ? qo.fhi : qo.flo;
-        const int64_t addr = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
-        a.ef[addr] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
-      }
-    }
+    __threadfence_block();  // slots + the dense e stores of step 1 before the quantiser's fix-ups
+    if (buf) ptx::named_arrive<kBarReady0 + 1>(kThreads);
+    else ptx::named_arrive<kBarReady0>(kThreads);
   }
 }
 
-template <bool BF16>
-cudaError_t launch_pipe(const CompressArgs& a, cudaStream_t s) {
+template <bool BF16, int KC, int IBC>
+cudaError_t launch_pipe_t(const CompressArgs& a, cudaStream_t s) {
   constexpr size_t smem = PipeSmem<BF16>::bytes;
-  cudaError_t e = cudaFuncSetAttribute(compress_pipe_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = compress_pipe_kernel<BF16, KC, IBC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_pipe_kernel<BF16>, kNT, smem)) !=
-      cudaSuccess)
-    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem)) != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.n_chunks) grid = a.n_chunks;
-  compress_pipe_kernel<BF16><<<(unsigned)grid, kNT, smem, s>>>(a);
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <bool BF16>
+cudaError_t launch_pipe(const CompressArgs& a, cudaStream_t s) {
+  if (a.g.k == 64 && a.g.ib == 12) return launch_pipe_t<BF16, 64, 12>(a, s);  // the paper's geometry
+  return launch_pipe_t<BF16, 0, 0>(a, s);
 }
 
 }  // namespace

@@ -78,3 +78,43 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 
 }  // namespace ptx
 }  // namespace slc
+
+namespace slc {
+namespace ptx {
+
+// 16-byte cp.async (LDGSTS), L2-only (.cg)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// arrive on `bar` once all of this thread's prior cp.async have completed
+// (no pending-count increment: the barrier's count includes these arrivals)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barriers (ids 1..15; 0 is __syncthreads); ids are immediates so
+// ptxas only reserves the barriers actually used
+template <int ID>
+__device__ __forceinline__ void named_sync(int nthreads) {
+  asm volatile("barrier.cta.sync.aligned %0, %1;" ::"n"(ID), "r"(nthreads) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void named_arrive(int nthreads) {
+  asm volatile("barrier.cta.arrive.aligned %0, %1;" ::"n"(ID), "r"(nthreads) : "memory");
+}
+// count of threads (of nthreads) with pred true; all of them wait
+template <int ID>
+__device__ __forceinline__ int named_count(int nthreads, bool pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+      "barrier.cta.red.popc.aligned.u32 %0, %1, %3, p;\n\t}"
+      : "=r"(r)
+      : "n"(ID), "r"((uint32_t)pred), "r"(nthreads)
+      : "memory");
+  return r;
+}
+
+}  // namespace ptx
+}  // namespace slc

@@ -22,6 +22,20 @@ __device__ __forceinline__ float warp_tree_sum(float u) {
   return u;
 }
 
+// sum over the NT threads of named barrier BAR
+template <int NT, int BAR>
+__device__ __forceinline__ int block_sum_named(int v, int* s_w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = __reduce_add_sync(kFull, v);
+  if (lane == 0) s_w[warp] = v;
+  asm volatile("barrier.cta.sync.aligned %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  int tot = 0;
+#pragma unroll
+  for (int i = 0; i < NT / 32; i++) tot += s_w[i];
+  asm volatile("barrier.cta.sync.aligned %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  return tot;
+}
+
 template <int NT>
 __device__ __forceinline__ int block_sum(int v, int* s_w) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -54,10 +68,14 @@ struct QuantOut {
 // ascending position order.  Computes the 2-bit quantiser of R#1 with the
 // fixed-order sums of R#13 and fp16 scales (R#14), writes the record (R#6) and
 // returns tau and the decoded scales.  selcode is scratch (k entries).
+// KC / IBC > 0 fix k / index_bits at compile time (the paper's 64 / 12),
+// which unrolls the slot loops and turns the packing divisions into shifts.
+template <int KC = 0, int IBC = 0>
 __device__ __forceinline__ QuantOut warp_quantize_pack(const uint32_t* selpos, const float* selval,
-                                                       uint32_t* selcode, int k, int k_eff, const Geom& g,
+                                                       uint32_t* selcode, int k_rt, int k_eff, const Geom& g,
                                                        uint32_t* rec, uint32_t* err) {
   const int lane = threadIdx.x & 31;
+  const int k = KC ? KC : k_rt;
   const int W = (k + 31) >> 5;
   float u = 0.0f;
   for (int m = 0; m < W; m++) {
@@ -92,7 +110,10 @@ __device__ __forceinline__ QuantOut warp_quantize_pack(const uint32_t* selpos, c
   if (lane == 0 && (isinf(q.flo) || isinf(q.fhi))) atomicOr(err, kErrScaleOverflow);
   const uint32_t scale_word = (uint32_t)__half_as_ushort(hlo) | ((uint32_t)__half_as_ushort(hhi) << 16);
   __syncwarp();
-  const int IW = g.idx_words, CW = g.code_words, RW = g.rec_words, ib = g.ib;
+  const int ib = IBC ? IBC : g.ib;
+  const int IW = (KC && IBC) ? (KC * IBC + 31) / 32 : g.idx_words;
+  const int CW = KC ? (2 * KC + 31) / 32 : g.code_words;
+  const int RW = IW + CW + 1;
   for (int wi = lane; wi < RW; wi += 32) {
     uint32_t word = 0;
     if (wi < IW) {
