@@ -323,66 +323,51 @@ def run_e2e(args, plan, shard, recs, stream):
 
 
 # --------------------------------------------------------------------------- oracle (CPU) arm
-def cpu_baseline(layout, R, dtype, seconds):
-    """The oracle as it stands, single-threaded, on a bounded sample of the
-    workload's chunks: compress of the own chunk + R-1 peers' records, then
-    aggregate + update — params/s extrapolated from chunks/s."""
+def cpu_baseline(layout, R, dtype, seconds, pool=256):
+    """The oracle as it stands (oracle/slco.c, single-threaded) on a bounded
+    sample of the workload: per chunk-step = compress the own chunk + aggregate
+    R records (own + R-1 peers) + outer update, over a deterministic pool of
+    `pool` chunks drawn across all tensors (peer records precomputed, untimed),
+    cycled until `seconds` of oracle time.  params/s = chunk params / time."""
     import numpy as np
 
     import oracle
     import slcgen
     g = oracle.geom()
     offs = np.cumsum([0] + [int(np.prod(s)) for _, s in layout])
-    # deterministic sample: every 97th tensor chunk, cycling through tensors
-    chunks = []
-    for ti, (_, shape) in enumerate(layout):
-        nc = oracle.tensor_chunks(shape, g)
-        for c in range(0, nc, max(1, nc // 8)):
-            chunks.append((ti, c))
+    allc = [(ti, c) for ti, (_, shape) in enumerate(layout) for c in range(oracle.tensor_chunks(shape, g))]
     rng = np.random.default_rng(0)
-    rng.shuffle(chunks)
-    done = 0
-    elems = 0
-    t0 = time.perf_counter()
-    work = 0.0
-    for ti, c in chunks:
-        shape = layout[ti][1]
-        off = oracle.chunk_offsets(shape, c, g)
+    pick = sorted(rng.choice(len(allc), size=min(pool, len(allc)), replace=False).tolist())
+    sample = []
+    for i in pick:
+        ti, c = allc[i]
+        off = oracle.chunk_offsets(layout[ti][1], c, g)
         G = offs[ti] + off
-        # inputs (generation excluded from timing)
-        ins = []
-        for r in range(R):
-            a = slcgen.generate_at(0, 0, r, G, dtype=dtype)
-            l = slcgen.generate_at(1, 0, r, G, dtype=dtype)
-            e = slcgen.generate_at(2, 0, r, G, warm_ef=True)
-            ins.append((a, l, e))
-        s = time.perf_counter()
-        recs = []
-        for r in range(R):
-            st, rec, en = oracle.compress_chunk(*ins[r], BETA, g)
-            recs.append(rec)
-        delta = oracle.aggregate_chunk(recs, len(off), g=g)
-        oracle.outer_update(ins[0][0], delta, ALPHA)
-        work += time.perf_counter() - s
-        done += 1
-        elems += len(off)
-        if work > seconds or time.perf_counter() - t0 > 4 * seconds:
-            break
-    # per outer step a peer compresses ONE payload (its own) and aggregates R: count 1 compress + 1 aggregate
-    # per chunk -> scale the R compresses down to 1
-    per_elem_s = work / elems
-    comp_share = None
-    # time one compress alone on the last chunk to split the cost
-    s = time.perf_counter()
-    for _ in range(5):
-        oracle.compress_chunk(*ins[0], BETA, g)
-    t_comp = (time.perf_counter() - s) / 5
-    t_chunk_total = work / done
-    t_step_chunk = t_chunk_total - (R - 1) * t_comp
-    v = (elems / done) / t_step_chunk
-    return {"value": v, "unit": "params/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} chunks of {len(layout)} tensors ({elems} params), R={R}, single-threaded C oracle, "
-                      f"{work:.1f}s; per-chunk = 1 compress + aggregate of R records + update"}
+        a = slcgen.generate_at(0, 0, 0, G, dtype=dtype)
+        l = slcgen.generate_at(1, 0, 0, G, dtype=dtype)
+        e = slcgen.generate_at(2, 0, 0, G, warm_ef=True)
+        peers = []
+        for r in range(1, R):
+            st, rec, _ = oracle.compress_chunk(a, slcgen.generate_at(1, 0, r, G, dtype=dtype),
+                                               slcgen.generate_at(2, 0, r, G, warm_ef=True), BETA, g)
+            peers.append(rec)
+        sample.append((a, l, e, peers, len(off)))
+    work, steps, params = 0.0, 0, 0
+    while work < seconds:
+        for a, l, e, peers, n in sample:
+            t0 = time.perf_counter()
+            st, rec, en = oracle.compress_chunk(a, l, e, BETA, g)
+            delta = oracle.aggregate_chunk([rec] + peers, n, g=g)
+            oracle.outer_update(a, delta, ALPHA)
+            work += time.perf_counter() - t0
+            steps += 1
+            params += n
+            if work >= seconds:
+                break
+    return {"value": params / work, "unit": "params/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} chunk-steps over a pool of {len(sample)} chunks drawn from all {len(layout)} tensors "
+                      f"({params} params), R={R}; per chunk: compress own + aggregate R records + update; "
+                      f"single-threaded C oracle, {work:.1f} s"}
 
 
 def run_reference(args):

@@ -61,26 +61,34 @@ template <bool BF16>
 __device__ __forceinline__ void prefetch_chunk(const CompressArgs& a, int64_t c, unsigned char* stage, uint64_t* bar,
                                                int t) {
   using S = PipeSmem<BF16>;
-  constexpr int PB = S::PB;
   const ChunkDesc d = a.chunks[c];
   if (d.len == kC) {
     const unsigned char* th = static_cast<const unsigned char*>(a.theta);
     const unsigned char* tl = static_cast<const unsigned char*>(a.theta_local);
     const unsigned char* ef = reinterpret_cast<const unsigned char*>(a.ef);
-    constexpr int EPP = 16 / PB;       // elements per 16-byte piece
-    constexpr int PP = kC / EPP;       // pieces per param array
+    // fp32 pieces: positions 4(t + 256u), u = 0..3 — the consumer's groups
+    const int64_t g0 = group_offset(d, t, 4);
+    const int64_t gs = d.ld ? 16 * (int64_t)d.ld : 4 * kNT;
 #pragma unroll
-    for (int m = t; m < PP; m += kNT) {
-      const int p = m * EPP;
-      const int64_t g = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
-      ptx::cp_async16(stage + S::arr_theta + (size_t)p * PB, th + g * PB);
-      ptx::cp_async16(stage + S::arr_tl + (size_t)p * PB, tl + g * PB);
-    }
-#pragma unroll
-    for (int m = t; m < kC / 4; m += kNT) {
-      const int p = 4 * m;
-      const int64_t g = d.ld ? d.base + (int64_t)(p >> 6) * d.ld + (p & 63) : d.base + p;
+    for (int u = 0; u < 4; u++) {
+      const int p = 4 * (u * kNT + t);
+      const int64_t g = g0 + u * gs;
       ptx::cp_async16(stage + S::arr_e + (size_t)p * 4, ef + g * 4);
+      if (!BF16) {
+        ptx::cp_async16(stage + S::arr_theta + (size_t)p * 4, th + g * 4);
+        ptx::cp_async16(stage + S::arr_tl + (size_t)p * 4, tl + g * 4);
+      }
+    }
+    if (BF16) {  // bf16 pieces of 8 elements: positions 8(t + 256u), u = 0..1
+      const int64_t h0 = d.ld ? d.base + (int64_t)(t >> 3) * d.ld + 8 * (t & 7) : d.base + 8 * t;
+      const int64_t hs = d.ld ? 32 * (int64_t)d.ld : 8 * kNT;
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int p = 8 * (u * kNT + t);
+        const int64_t g = h0 + u * hs;
+        ptx::cp_async16(stage + S::arr_theta + (size_t)p * 2, th + g * 2);
+        ptx::cp_async16(stage + S::arr_tl + (size_t)p * 2, tl + g * 2);
+      }
     }
   }
   ptx::cp_async_arrive_noinc(bar);  // partial chunk: consumers read global memory directly
@@ -100,7 +108,9 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
   uint32_t* selcode = reinterpret_cast<uint32_t*>(smem + S::off_code);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::off_bar);
   __shared__ int s_ncand;
+  __shared__ uint32_t s_T;
   __shared__ int s_w[kNT / 32];
+  __shared__ __align__(16) uint32_t slm[kNT];
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t G = gridDim.x, n = a.n_chunks;
@@ -163,18 +173,17 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
     const int k_eff = full ? k : max(1, (k * len) / kC);
 
     // ---- 1. inputs -> b; dense e <- b -------------------------------------------
+    // key2(b) = |b| bits << 1 | 1: order-preserving on |b|, 0 marks a missing position
     ptx::mbar_wait(&bars[s], par);
     float b[16];
     uint32_t lm = 0;
-    bool bad = false;
+    if (full) {
+      const int64_t off0 = group_offset(d, t, 4);
+      const int64_t vstride = d.ld ? 16 * (int64_t)d.ld : 4 * kNT;  // element step between groups v
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
-      const int q = v * kNT + t;
-      const int p0 = 4 * q;
-      const int64_t off = group_offset(d, q, 4);
-      float av[4], lv[4], ev[4];
-      int nv = 4;
-      if (full) {
+      for (int v = 0; v < 4; v++) {
+        const int p0 = 4 * (v * kNT + t);
+        float av[4], lv[4];
         if (BF16) {
           const uint2 ua = *reinterpret_cast<const uint2*>(stage + S::arr_theta + 2 * p0);
           const uint2 ul = *reinterpret_cast<const uint2*>(stage + S::arr_tl + 2 * p0);
@@ -189,46 +198,68 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
           lv[0] = fl.x; lv[1] = fl.y; lv[2] = fl.z; lv[3] = fl.w;
         }
         const float4 fe = *reinterpret_cast<const float4*>(stage + S::arr_e + 4 * p0);
-        ev[0] = fe.x; ev[1] = fe.y; ev[2] = fe.z; ev[3] = fe.w;
-      } else {
-        nv = valid_in_group(p0, len);
+        const float ev[4] = {fe.x, fe.y, fe.z, fe.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) b[4 * v + j] = __fmaf_rn(a.beta, ev[j], __fsub_rn(av[j], lv[j]));
+        *reinterpret_cast<float4*>(a.ef + off0 + v * vstride) =
+            make_float4(b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) lm = max(lm, max(key2_of(b[j]), key2_of(b[j + 1])));
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int q = v * kNT + t;
+        const int p0 = 4 * q;
+        const int64_t off = group_offset(d, q, 4);
+        const int nv = valid_in_group(p0, len);
+        float av[4], lv[4], ev[4];
         load_param4<BF16>(a.theta, off, nv, av);
         load_param4<BF16>(a.theta_local, off, nv, lv);
         load_f32x4(a.ef, off, nv, ev);
-      }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const float bb = __fmaf_rn(a.beta, ev[j], __fsub_rn(av[j], lv[j]));
-        b[4 * v + j] = bb;
-        const uint32_t key = (j < nv) ? key_of(bb) : 0u;
-        bad |= key > 0x7F800000u;
-        lm = max(lm, key);
+        for (int j = 0; j < 4; j++) {
+          b[4 * v + j] = __fmaf_rn(a.beta, ev[j], __fsub_rn(av[j], lv[j]));
+          if (j < nv) lm = max(lm, key2_of(b[4 * v + j]));
+        }
+        store_f32x4(a.ef, off, nv, &b[4 * v]);
       }
-      if (full) *reinterpret_cast<float4*>(a.ef + off) = make_float4(b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3]);
-      else store_f32x4(a.ef, off, nv, &b[4 * v]);
     }
-    if (bad) atomicOr(a.err, kErrNonFinite);
+    if (lm >= 0xFF000001u) atomicOr(a.err, kErrNonFinite);  // |b| = inf or NaN (max key wins)
+    slm[t] = lm;
 
     // ---- 2. lower bound T from the thread maxima; refill the stage ---------------
-    uint32_t T = 0;
-    if (ptx::named_count<kBarCompute>(kNT, lm >= (1u << 30)) >= k_eff) T = 1u << 30;
+    ptx::named_sync<kBarCompute>(kNT);  // every thread is done with stage s
     if (c + 2 * G < n) prefetch_chunk<BF16>(a, c + 2 * G, stage, &bars[s], t);
     if (t >= kNT - kC / 32) { sbit[t - (kNT - kC / 32)] = 0u; stie[t - (kNT - kC / 32)] = 0u; }
-    if (t == 0) s_ncand = 0;
+    if (t == 32) s_ncand = 0;
+    if (warp == 0) {
+      // largest T (bits 31..17) with >= k_eff of the 256 thread maxima >= T
+      const uint4 m0 = *reinterpret_cast<const uint4*>(slm + 8 * lane);
+      const uint4 m1 = *reinterpret_cast<const uint4*>(slm + 8 * lane + 4);
+      uint32_t T = 0;
 #pragma unroll
-    for (int bit = 29; bit >= 16; --bit) {
-      const uint32_t Tp = T | (1u << bit);
-      if (ptx::named_count<kBarCompute>(kNT, lm >= Tp) >= k_eff) T = Tp;
+      for (int bit = 31; bit >= 17; --bit) {
+        const uint32_t Tp = T | (1u << bit);
+        const int c8 = (m0.x >= Tp) + (m0.y >= Tp) + (m0.z >= Tp) + (m0.w >= Tp) + (m1.x >= Tp) + (m1.y >= Tp) +
+                       (m1.z >= Tp) + (m1.w >= Tp);
+        if (__reduce_add_sync(kFull, c8) >= k_eff) T = Tp;
+      }
+      if (lane == 0) s_T = T;
     }
-    const uint32_t Tc = max(T, 1u);
+    ptx::named_sync<kBarCompute>(kNT);
+    const uint32_t Tc = max(s_T, 1u);
 
     // ---- 3. candidates -----------------------------------------------------------------
-    int cnt = 0;
+    uint32_t mask = 0;
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
-      cnt += ((full || p < len) && key_of(b[j]) >= Tc);
+    for (int j = 0; j < 16; j++) mask |= (uint32_t)(key2_of(b[j]) >= Tc) << j;
+    if (!full) {  // missing positions of a partial chunk are never candidates
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if (4 * ((j >> 2) * kNT + t) + (j & 3) >= len) mask &= ~(1u << j);
     }
+    const int cnt = __popc(mask);
     const int incl = warp_excl_scan(cnt) + cnt;
     int wbase = 0;
     if (lane == 31) wbase = atomicAdd(&s_ncand, incl);
@@ -236,14 +267,15 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
     int slot = wbase + incl - cnt;
 #pragma unroll
     for (int j = 0; j < 16; j++) {
-      const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
-      const uint32_t key = key_of(b[j]);
-      if ((full || p < len) && key >= Tc) {
-        if (slot < kMaxCand) {
-          scand[slot] = ((uint64_t)key << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
-          candb[slot] = b[j];
+      if (__ballot_sync(kFull, (mask >> j) & 1u)) {  // warp-uniform skip: candidates are sparse
+        if ((mask >> j) & 1u) {
+          const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
+          if (slot < kMaxCand) {
+            scand[slot] = ((uint64_t)key2_of(b[j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
+            candb[slot] = b[j];
+          }
+          slot++;
         }
-        slot++;
       }
     }
     ptx::named_sync<kBarCompute>(kNT);
@@ -273,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
 #pragma unroll
         for (int j = 0; j < 16; j++) {
           const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
-          cc += (p < len && key_of(b[j]) >= Tp);
+          cc += (p < len && key2_of(b[j]) >= Tp);
         }
         if (block_sum_named<kNT, kBarCompute>(cc, s_w) >= k_eff) Kth = Tp;
       }
@@ -282,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 2) compress_pipe_kernel(const Compre
       for (int j = 0; j < 16; j++) {
         const int p = 4 * ((j >> 2) * kNT + t) + (j & 3);
         if (p < len) {
-          const uint32_t key = key_of(b[j]);
+          const uint32_t key = key2_of(b[j]);
           if (key > Kth) { atomicOr(&sbit[p >> 5], 1u << (p & 31)); gt++; }
           else if (key == Kth) atomicOr(&stie[p >> 5], 1u << (p & 31));
         }

@@ -12,6 +12,8 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // key(b) = |b| bits + 1 (order-preserving for finite b; 0 = missing position)
 __device__ __forceinline__ uint32_t key_of(float b) { return (__float_as_uint(b) & 0x7FFFFFFFu) + 1u; }
+// key2(b) = |b| bits << 1 | 1 — same order, one instruction (LEA); 0 = missing
+__device__ __forceinline__ uint32_t key2_of(float b) { return (__float_as_uint(b) << 1) | 1u; }
 
 // xor butterfly of __fadd_rn: lane l < d adds u_{l+d} exactly as the oracle's
 // tree (R#13); the partner lane computes the same commutative sum, so every
