@@ -286,8 +286,8 @@ cudaError_t launch_compress_simple(const CompressArgs& a, int bf16, cudaStream_t
 cudaError_t launch_compress(const CompressArgs& a, int bf16, cudaStream_t s) {
   if (a.n_chunks == 0) return cudaSuccess;
   switch (a.g.C) {
-    case 1024: return bf16 ? launch_one<1024, true>(a, s) : launch_one<1024, false>(a, s);
-    case 4096: return launch_compress_pipe(a, bf16, s);
+    case 1024:
+    case 4096: return launch_compress_warp(a, bf16, s);
     case 16384: return bf16 ? launch_one<16384, true>(a, s) : launch_one<16384, false>(a, s);
   }
   return cudaErrorInvalidValue;

@@ -65,8 +65,8 @@ struct AggArgs {
 cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one CTA per chunk, any compiled C (reference kernel for the pipelined one)
 cudaError_t launch_compress_simple(const CompressArgs& a, int param_bf16, cudaStream_t s);
-// persistent, bulk-copy double-buffered kernel for C = 4096
-cudaError_t launch_compress_pipe(const CompressArgs& a, int param_bf16, cudaStream_t s);
+// one warp per chunk, no block-level synchronisation (C = 1024, 4096)
+cudaError_t launch_compress_warp(const CompressArgs& a, int param_bf16, cudaStream_t s);
 cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
 bool compress_supported(int C);
 
