@@ -36,6 +36,9 @@ __device__ __forceinline__ uint32_t rec_index(const uint32_t* rec, int j, int ib
   return (uint32_t)(two >> sh) & ((1u << ib) - 1u);
 }
 
+// records of the chunk are staged in shared memory when they fit
+constexpr int kRecSmemWords = 8192;  // 32 KB
+
 template <int C, bool BF16>
 __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
   using K = ChunkCfg<C>;
@@ -44,24 +47,46 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long* acc = reinterpret_cast<long long*>(smem);  // exact path
   double* accd = reinterpret_cast<double*>(smem);       // weighted path
+  uint32_t* srec = reinterpret_cast<uint32_t*>(smem + sizeof(long long) * C);
 
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t chunk = blockIdx.x;
   const ChunkDesc d = a.chunks[chunk];
   const int len = d.len;
   const int mode = a.mode;
 
+  // theta (and agg) first: their HBM latency overlaps the decode below
+  float th[16], dl[16];
+  int64_t off[4];
+  int nvs[4];
+#pragma unroll
+  for (int v = 0; v < 4; v++) {
+    const int q = v * NT + t;
+    off[v] = group_offset(d, q, RPQ_SHIFT);
+    nvs[v] = valid_in_group(4 * q, len);
+    if (mode != kAggOnly) load_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
+    if (mode == kUpdateFromAgg) load_f32x4(a.agg, off[v], nvs[v], &dl[4 * v]);
+  }
+
   if (mode != kUpdateFromAgg) {
     const int k_eff = max(1, (a.g.k * len) / C);
     const int RW = a.g.rec_words, IW = a.g.idx_words, ib = a.g.ib;
+    const bool staged = a.R * RW <= kRecSmemWords;
+    if (staged) {
+      for (int r = warp; r < a.R; r += NT / 32) {
+        const uint32_t* rec = a.rec[r] + chunk * RW;
+        for (int w = lane; w < RW; w += 32) srec[r * RW + w] = __ldcs(rec + w);
+      }
+    }
     for (int i = t; i < C / 2; i += NT) reinterpret_cast<longlong2*>(acc)[i] = make_longlong2(0, 0);
     __syncthreads();
     bool bad = false;
     if (!a.weighted) {
       const int total = a.R * k_eff;
       for (int s = t; s < total; s += NT) {
-        const int r = s / k_eff, j = s - r * k_eff;
-        const uint32_t* rec = a.rec[r] + chunk * RW;
+        const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
+        const int j = s - r * k_eff;
+        const uint32_t* rec = staged ? srec + r * RW : a.rec[r] + chunk * RW;
         const uint32_t p = rec_index(rec, j, ib);
         const uint32_t code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
         const uint32_t sw = rec[RW - 1];
@@ -73,7 +98,7 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
       }
     } else if (t < 32) {
       for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
-        const uint32_t* rec = a.rec[i] + chunk * RW;
+        const uint32_t* rec = staged ? srec + i * RW : a.rec[i] + chunk * RW;
         const double w = (double)a.w[i];
         const uint32_t sw = rec[RW - 1];
         for (int j = t; j < k_eff; j += 32) {
@@ -90,42 +115,39 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     }
     if (bad) atomicOr(a.err, kErrNonFinite);
     __syncthreads();
-  }
-
-  const double invR = a.invR;
-  const float alpha = a.alpha;
+    const double invR = a.invR;
 #pragma unroll
-  for (int v = 0; v < 4; v++) {
-    const int q = v * NT + t;
-    const int p0 = 4 * q;
-    const int n = valid_in_group(p0, len);
-    if (n == 0) continue;
-    const int64_t off = group_offset(d, q, RPQ_SHIFT);
-    float delta[4];
-    if (mode == kUpdateFromAgg) {
-      load_f32x4(a.agg, off, n, delta);
-    } else {
+    for (int v = 0; v < 4; v++) {
+      const int p0 = 4 * (v * NT + t);
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const double x = a.weighted ? accd[p0 + j] : __dmul_rn((double)acc[p0 + j], 0x1p-24);
-        delta[j] = __double2float_rn(__dmul_rn(x, invR));
+        dl[4 * v + j] = __double2float_rn(__dmul_rn(x, invR));
       }
     }
-    if (mode == kAggOnly) {
-      store_f32x4(a.agg, off, n, delta);
-    } else {
-      float th[4];
-      load_param4<BF16>(a.theta, off, n, th);
+  }
+
+  const float alpha = a.alpha;
 #pragma unroll
-      for (int j = 0; j < 4; j++) th[j] = __fmaf_rn(-alpha, delta[j], th[j]);
-      store_param4<BF16>(a.theta, off, n, th);
+  for (int v = 0; v < 4; v++) {
+    if (nvs[v] == 0) continue;
+    if (mode == kAggOnly) {
+      store_f32x4(a.agg, off[v], nvs[v], &dl[4 * v]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) th[4 * v + j] = __fmaf_rn(-alpha, dl[4 * v + j], th[4 * v + j]);
+      store_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
     }
   }
 }
 
 template <int C, bool BF16>
 cudaError_t launch_one(const AggArgs& a, cudaStream_t s) {
-  const size_t smem = a.mode == kUpdateFromAgg ? 0 : sizeof(long long) * C;
+  size_t smem = 0;
+  if (a.mode != kUpdateFromAgg) {
+    smem = sizeof(long long) * C;
+    if ((size_t)a.R * a.g.rec_words <= (size_t)kRecSmemWords) smem += sizeof(uint32_t) * a.R * a.g.rec_words;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(aggregate_kernel<C, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

@@ -63,6 +63,10 @@ __device__ __forceinline__ float absmax_nan(float m, float x) {
   return r;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // element offset of the 4-position group q of chunk d
 template <int RPQ_SHIFT>
 __device__ __forceinline__ int64_t goff(const ChunkDesc& d, int q) {
@@ -71,6 +75,19 @@ __device__ __forceinline__ int64_t goff(const ChunkDesc& d, int q) {
 
 __device__ __forceinline__ int64_t pos_off(const ChunkDesc& d, int p, int B) {
   return d.ld ? d.base + (int64_t)(p / B) * d.ld + (p % B) : d.base + p;
+}
+
+// L2 prefetch of pass u of chunk d (the lane's 4 groups of theta, theta_local, e)
+template <int RPQ_SHIFT, bool BF16>
+__device__ __forceinline__ void prefetch_pass(const CompressArgs& a, const ChunkDesc& d, int u, int lane) {
+  const int pb = BF16 ? 2 : 4;
+#pragma unroll
+  for (int v = 0; v < 4; v++) {
+    const int64_t off = goff<RPQ_SHIFT>(d, 128 * u + 32 * v + lane);
+    prefetch_l2(static_cast<const char*>(a.theta) + off * pb);
+    prefetch_l2(static_cast<const char*>(a.theta_local) + off * pb);
+    prefetch_l2(a.ef + off);
+  }
 }
 
 template <int C, bool BF16, int KC, int IBC>
@@ -83,8 +100,23 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int k = KC ? KC : a.g.k;
 
+#ifndef SLC_PD
+#define SLC_PD 2
+#endif
+  constexpr int PD = SLC_PD;  // L2 prefetch distance in passes
+  {
+    const int64_t c0 = (int64_t)blockIdx.x * kWarps + warp;
+    if (c0 < a.n_chunks) {
+      const ChunkDesc d0 = a.chunks[c0];
+      if (d0.len == C)
+        for (int u = 0; u < PD && u < NP; u++) prefetch_pass<K::RPQ_SHIFT, BF16>(a, d0, u, lane);
+    }
+  }
   for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < a.n_chunks; c += W) {
     const ChunkDesc d = a.chunks[c];
+    const bool has_next = c + W < a.n_chunks;
+    ChunkDesc dn = d;
+    if (has_next) dn = a.chunks[c + W];
     const int len = d.len;
     const bool full = len == C;
     const int k_eff = full ? k : max(1, (k * len) / C);
@@ -93,6 +125,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
     uint32_t gk[NP];
 #pragma unroll
     for (int u = 0; u < NP; u++) {
+      // keep PD passes of loads in flight through L2 (this chunk, then the next one)
+      if (u + PD < NP) {
+        if (full) prefetch_pass<K::RPQ_SHIFT, BF16>(a, d, u + PD, lane);
+      } else if (has_next && dn.len == C && u + PD - NP < NP) {
+        prefetch_pass<K::RPQ_SHIFT, BF16>(a, dn, u + PD - NP, lane);
+      }
       float b[16];
       float gm = 0.0f;
       int nvalid = 0;

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslc.so")
+LIB_PATH = os.environ.get("SLC_LIB") or os.path.join(_HERE, "libslc.so")  # SLC_LIB: tuning variants
 
 OK, INVALID_ARGUMENT, INVALID_DATA, STALE, CUDA_ERROR, UNSUPPORTED = range(6)
 F32, BF16 = 0, 1

@@ -1,0 +1,7 @@
+# time compress/update of each libslc variant in build/variants (bench.py, short run)
+mkdir -p gpurun_out
+for so in build/variants/*.so; do
+  n=$(basename $so .so)
+  SLC_LIB=$so timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/var_$n.log 2>&1
+  echo "$n $(python -c "import json,sys; d=json.loads(open('gpurun_out/var_$n.log').read().strip().splitlines()[-1]); print(d['kernels']['compress_ms'], d['kernels']['fused_update_ms'], d['ms_per_step'])" 2>&1 | tail -1)"
+done
