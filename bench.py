@@ -30,6 +30,7 @@ WORKLOADS = {
     "covenant-72b": ("covenant-72b", 20, "f32"),   # BASELINE configs[3]
     "llama2-7b": ("llama2-7b", 20, "f32"),         # BASELINE configs[4] base point
     "1m": ("1m-2d", 1, "f32"),                     # BASELINE configs[0]
+    "flat-1b": ("flat-1b", 8, "f32"),              # bandwidth probe (contiguous chunks)
 }
 
 BETA = 0.95

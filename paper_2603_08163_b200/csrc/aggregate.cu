@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
   const int len = d.len;
   const int mode = a.mode;
 
-  // theta (and agg) first: their HBM latency overlaps the decode below
   float th[16], dl[16];
   int64_t off[4];
   int nvs[4];
@@ -64,10 +63,31 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     const int q = v * NT + t;
     off[v] = group_offset(d, q, RPQ_SHIFT);
     nvs[v] = valid_in_group(4 * q, len);
+  }
+#ifdef SLC_AGG_THETA_FIRST
+  // theta (and agg) first: their HBM latency overlaps the decode below
+#pragma unroll
+  for (int v = 0; v < 4; v++) {
     if (mode != kAggOnly) load_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
     if (mode == kUpdateFromAgg) load_f32x4(a.agg, off[v], nvs[v], &dl[4 * v]);
   }
+#else
+  if (mode == kUpdateFromAgg) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      load_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
+      load_f32x4(a.agg, off[v], nvs[v], &dl[4 * v]);
+    }
+  }
+#endif
 
+#ifdef SLC_STREAM_ONLY  // bandwidth probe: theta read + write only (tools/, never shipped)
+  if (mode == kFused) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) store_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
+    return;
+  }
+#endif
   if (mode != kUpdateFromAgg) {
     const int k_eff = max(1, (a.g.k * len) / C);
     const int RW = a.g.rec_words, IW = a.g.idx_words, ib = a.g.ib;
@@ -127,6 +147,12 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     }
   }
 
+#ifndef SLC_AGG_THETA_FIRST
+  if (mode == kFused) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) load_param4<BF16>(a.theta, off[v], nvs[v], &th[4 * v]);
+  }
+#endif
   const float alpha = a.alpha;
 #pragma unroll
   for (int v = 0; v < 4; v++) {

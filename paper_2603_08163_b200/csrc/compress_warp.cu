@@ -51,20 +51,29 @@ struct WarpScratch {
   uint64_t cand[WarpCfg<C>::CAP];
   float candb[WarpCfg<C>::CAP];
   uint32_t bit[WarpCfg<C>::BW];
+  uint32_t wpre[WarpCfg<C>::BW];
   uint32_t hist[256];                     // fallback histogram; also the group list in step B
   uint32_t selpos[kMaxK];
   float selval[kMaxK];
   uint32_t code[kMaxK];
 };
 
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void st_f32x4_evict_last(float* ptr, float x, float y, float z, float w, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(x), "f"(y), "f"(z),
+               "f"(w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ float absmax_nan(float m, float x) {
   float r;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(m), "f"(fabsf(x)));
   return r;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // element offset of the 4-position group q of chunk d
@@ -77,19 +86,6 @@ __device__ __forceinline__ int64_t pos_off(const ChunkDesc& d, int p, int B) {
   return d.ld ? d.base + (int64_t)(p / B) * d.ld + (p % B) : d.base + p;
 }
 
-// L2 prefetch of pass u of chunk d (the lane's 4 groups of theta, theta_local, e)
-template <int RPQ_SHIFT, bool BF16>
-__device__ __forceinline__ void prefetch_pass(const CompressArgs& a, const ChunkDesc& d, int u, int lane) {
-  const int pb = BF16 ? 2 : 4;
-#pragma unroll
-  for (int v = 0; v < 4; v++) {
-    const int64_t off = goff<RPQ_SHIFT>(d, 128 * u + 32 * v + lane);
-    prefetch_l2(static_cast<const char*>(a.theta) + off * pb);
-    prefetch_l2(static_cast<const char*>(a.theta_local) + off * pb);
-    prefetch_l2(a.ef + off);
-  }
-}
-
 template <int C, bool BF16, int KC, int IBC>
 __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const CompressArgs a) {
   using K = WarpCfg<C>;
@@ -99,24 +95,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
   WarpScratch<C>& ws = reinterpret_cast<WarpScratch<C>*>(smem_raw)[warp];
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int k = KC ? KC : a.g.k;
+  const uint64_t pol_last = l2_policy_evict_last();
 
-#ifndef SLC_PD
-#define SLC_PD 2
-#endif
-  constexpr int PD = SLC_PD;  // L2 prefetch distance in passes
-  {
-    const int64_t c0 = (int64_t)blockIdx.x * kWarps + warp;
-    if (c0 < a.n_chunks) {
-      const ChunkDesc d0 = a.chunks[c0];
-      if (d0.len == C)
-        for (int u = 0; u < PD && u < NP; u++) prefetch_pass<K::RPQ_SHIFT, BF16>(a, d0, u, lane);
-    }
-  }
   for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < a.n_chunks; c += W) {
     const ChunkDesc d = a.chunks[c];
-    const bool has_next = c + W < a.n_chunks;
-    ChunkDesc dn = d;
-    if (has_next) dn = a.chunks[c + W];
     const int len = d.len;
     const bool full = len == C;
     const int k_eff = full ? k : max(1, (k * len) / C);
@@ -125,12 +107,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
     uint32_t gk[NP];
 #pragma unroll
     for (int u = 0; u < NP; u++) {
-      // keep PD passes of loads in flight through L2 (this chunk, then the next one)
-      if (u + PD < NP) {
-        if (full) prefetch_pass<K::RPQ_SHIFT, BF16>(a, d, u + PD, lane);
-      } else if (has_next && dn.len == C && u + PD - NP < NP) {
-        prefetch_pass<K::RPQ_SHIFT, BF16>(a, dn, u + PD - NP, lane);
-      }
       float b[16];
       float gm = 0.0f;
       int nvalid = 0;
@@ -149,12 +125,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
           gm = absmax_nan(gm, b[4 * v + j]);  // missing positions hold b = 0: never above a valid max
         }
         nvalid += nv;
-        if (full) *reinterpret_cast<float4*>(a.ef + off) = make_float4(b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3]);
+        // e <- b, kept L2-resident (evict_last) until the candidate groups are re-read below
+        if (full) st_f32x4_evict_last(a.ef + off, b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3], pol_last);
         else store_f32x4(a.ef, off, nv, &b[4 * v]);
       }
       gk[u] = nvalid ? key2_of(gm) : 0u;
     }
 
+#ifdef SLC_STREAM_ONLY  // bandwidth probe: the streaming pass alone (tools/, never shipped)
+    if (lane == 0 && gk[0] == 0x12345u) a.records[c] = gk[1];
+    continue;
+#endif
     // ---- S. lower bound T ----------------------------------------------------------
     uint32_t gmaxk = 0;
 #pragma unroll
@@ -271,6 +252,29 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
           atomicOr(&ws.bit[p >> 5], 1u << (p & 31));
         }
       }
+      __syncwarp();
+      // ---- P. slot = selected positions below p (bitmap prefix) ----------------------------
+      {
+        constexpr int WPL = K::BW / 32;
+        uint32_t w[WPL];
+        int cw = 0;
+#pragma unroll
+        for (int x = 0; x < WPL; x++) { w[x] = ws.bit[WPL * lane + x]; cw += __popc(w[x]); }
+        int pre = warp_excl_scan(cw);
+#pragma unroll
+        for (int x = 0; x < WPL; x++) { ws.wpre[WPL * lane + x] = (uint32_t)pre; pre += __popc(w[x]); }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < K::CAP / 32; m++) {
+        const int ci = lane + 32 * m;
+        if (m < NM && ci < M && rank[m] < k_eff) {
+          const uint32_t p = 0xFFFFu - (uint32_t)(mine[m] & 0xFFFFu);
+          const int sl = (int)ws.wpre[p >> 5] + __popc(ws.bit[p >> 5] & ((1u << (p & 31)) - 1u));
+          ws.selpos[sl] = p;
+          ws.selval[sl] = ws.candb[ci];
+        }
+      }
     } else {
       // ---- fallback: exact k_eff-th largest key by 4 rounds of 8-bit radix select ----
       uint32_t Kth = 0;
@@ -365,11 +369,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
           taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
         }
       }
-    }
-    __syncwarp();
-
-    // ---- P. slots in ascending position -----------------------------------------------
-    {
+      __syncwarp();
+      // slots in ascending position; values re-read from e (b, written in step A)
       constexpr int WPL = K::BW / 32;
       uint32_t w[WPL];
       int cw = 0;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
           const int p = 32 * (WPL * lane + x) + bp;
           if (pre < kMaxK) {
             ws.selpos[pre] = (uint32_t)p;
-            ws.selval[pre] = a.ef[pos_off(d, p, K::B)];  // b (dense e was written in step A)
+            ws.selval[pre] = a.ef[pos_off(d, p, K::B)];
           }
           pre++;
         }
