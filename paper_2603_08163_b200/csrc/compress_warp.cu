@@ -35,6 +35,15 @@ namespace slc {
 namespace {
 
 constexpr int kWarps = 8;  // warps per CTA
+#ifndef SLC_PFN
+#define SLC_PFN 0  // passes of the NEXT chunk prefetched into L2 when a warp leaves its streaming pass
+#endif
+#ifndef SLC_A2
+#define SLC_A2 0   // 1: phase A issues the loads of two passes before consuming them
+#endif
+#ifndef SLC_MINB
+#define SLC_MINB 3  // CTAs per SM the register budget is sized for
+#endif
 
 template <int C>
 struct WarpCfg {
@@ -70,6 +79,8 @@ __device__ __forceinline__ void st_f32x4_evict_last(float* ptr, float x, float y
                : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ float absmax_nan(float m, float x) {
   float r;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(m), "f"(fabsf(x)));
@@ -87,7 +98,7 @@ __device__ __forceinline__ int64_t pos_off(const ChunkDesc& d, int p, int B) {
 }
 
 template <int C, bool BF16, int KC, int IBC>
-__global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const CompressArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, SLC_MINB) compress_warp_kernel(const CompressArgs a) {
   using K = WarpCfg<C>;
   constexpr int NP = K::NP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -104,37 +115,83 @@ __global__ void __launch_bounds__(kWarps * 32, 3) compress_warp_kernel(const Com
     const int k_eff = full ? k : max(1, (k * len) / C);
 
     // ---- A. stream inputs, b, dense e <- b, group maxima -------------------------
+    // All loads of a pass (12 x 128-bit per lane; PB passes with SLC_A2) are
+    // issued before any store: e may alias nothing here, but the compiler
+    // cannot know that, so the order is spelled out.
     uint32_t gk[NP];
+    constexpr int PB = SLC_A2 ? 2 : 1;
 #pragma unroll
-    for (int u = 0; u < NP; u++) {
-      float b[16];
-      float gm = 0.0f;
-      int nvalid = 0;
+    for (int u0 = 0; u0 < NP; u0 += PB) {
+      float av[PB][16], lv[PB][16], ev[PB][16];
+      if (full) {
 #pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const int q = 128 * u + 32 * v + lane;
-        const int64_t off = goff<K::RPQ_SHIFT>(d, q);
-        const int nv = full ? 4 : valid_in_group(4 * q, len);
-        float av[4], lv[4], ev[4];
-        load_param4<BF16>(a.theta, off, nv, av);
-        load_param4<BF16>(a.theta_local, off, nv, lv);
-        load_f32x4(a.ef, off, nv, ev);
+        for (int h = 0; h < PB; h++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          b[4 * v + j] = __fmaf_rn(a.beta, ev[j], __fsub_rn(av[j], lv[j]));
-          gm = absmax_nan(gm, b[4 * v + j]);  // missing positions hold b = 0: never above a valid max
-        }
-        nvalid += nv;
-        // e <- b, kept L2-resident (evict_last) until the candidate groups are re-read below
-        if (full) st_f32x4_evict_last(a.ef + off, b[4 * v], b[4 * v + 1], b[4 * v + 2], b[4 * v + 3], pol_last);
-        else store_f32x4(a.ef, off, nv, &b[4 * v]);
+          for (int v = 0; v < 4; v++) {
+            const int64_t off = goff<K::RPQ_SHIFT>(d, 128 * (u0 + h) + 32 * v + lane);
+            load_param4<BF16>(a.theta, off, 4, &av[h][4 * v]);
+            load_param4<BF16>(a.theta_local, off, 4, &lv[h][4 * v]);
+            load_f32x4(a.ef, off, 4, &ev[h][4 * v]);
+          }
+      } else {
+#pragma unroll
+        for (int h = 0; h < PB; h++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) {
+            const int q = 128 * (u0 + h) + 32 * v + lane;
+            const int64_t off = goff<K::RPQ_SHIFT>(d, q);
+            const int nv = valid_in_group(4 * q, len);
+            load_param4<BF16>(a.theta, off, nv, &av[h][4 * v]);
+            load_param4<BF16>(a.theta_local, off, nv, &lv[h][4 * v]);
+            load_f32x4(a.ef, off, nv, &ev[h][4 * v]);
+          }
       }
-      gk[u] = nvalid ? key2_of(gm) : 0u;
+#pragma unroll
+      for (int h = 0; h < PB; h++) {
+        float gm = 0.0f;
+#pragma unroll
+        for (int x = 0; x < 16; x++) {
+          av[h][x] = __fmaf_rn(a.beta, ev[h][x], __fsub_rn(av[h][x], lv[h][x]));  // b
+          gm = absmax_nan(gm, av[h][x]);  // missing positions hold b = 0: never above a valid max
+        }
+        int nvalid = 4 * 4;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int q = 128 * (u0 + h) + 32 * v + lane;
+          const int64_t off = goff<K::RPQ_SHIFT>(d, q);
+          const float* b = &av[h][4 * v];
+          // e <- b, kept L2-resident (evict_last) until the candidate groups are re-read below
+          if (full) {
+            st_f32x4_evict_last(a.ef + off, b[0], b[1], b[2], b[3], pol_last);
+          } else {
+            const int nv = valid_in_group(4 * q, len);
+            nvalid -= 4 - nv;
+            store_f32x4(a.ef, off, nv, b);
+          }
+        }
+        gk[u0 + h] = nvalid ? key2_of(gm) : 0u;
+      }
     }
 
 #ifdef SLC_STREAM_ONLY  // bandwidth probe: the streaming pass alone (tools/, never shipped)
     if (lane == 0 && gk[0] == 0x12345u) a.records[c] = gk[1];
     continue;
+#endif
+#if SLC_PFN > 0
+    if (c + W < a.n_chunks) {  // the next chunk's first passes travel to L2 while this warp selects
+      const ChunkDesc dn = a.chunks[c + W];
+      if (dn.len == C) {
+#pragma unroll
+        for (int u = 0; u < SLC_PFN; u++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) {
+            const int64_t off = goff<K::RPQ_SHIFT>(dn, 128 * u + 32 * v + lane);
+            prefetch_l2(static_cast<const char*>(a.theta) + off * (BF16 ? 2 : 4));
+            prefetch_l2(static_cast<const char*>(a.theta_local) + off * (BF16 ? 2 : 4));
+            prefetch_l2(a.ef + off);
+          }
+      }
+    }
 #endif
     // ---- S. lower bound T ----------------------------------------------------------
     uint32_t gmaxk = 0;
