@@ -1,491 +1,84 @@
-// compress_warp.cu — slc_compress, one WARP per chunk, software-pipelined
-// (Eq. 1 of PAPER.md; chunking P:88; C, k P:176).
+// compress_warp.cu — slc_compress, one WARP per chunk, reading its chunk
+// straight from global memory (Eq. 1 of PAPER.md).  Used for
+// C = 1024 and as the general path; the paper's C = 4096 runs the TMA-fed
+// kernel of compress_tma.cu.
 //
-// Every warp is an independent chunk worker (CTAs of 8 warps, no block-level
-// synchronisation anywhere: only __syncwarp, shuffles and warp reductions).
-// Warp w of the grid walks chunks w, w+W, w+2W, ...  Its loop body streams
-// chunk i in NP passes and, between issuing a pass's loads and consuming
-// them, runs one stage of the selection of chunk i-1 — so the load latency of
-// the stream is covered by the selection work, and every warp keeps a pass of
-// loads (6 KB) in flight nearly all the time.
-//
-// Stream (chunk i), pass u: lane l owns positions 4q..4q+3 for
-// q = 128u + 32v + l (v = 0..3) — each 128-bit load of the warp covers two
-// whole 256-byte rows of a 64x64 block (or 512 contiguous bytes of a flat
-// chunk).  d = theta - theta_local, b = fma(beta, e, d) (R#12); e <- b is
-// stored densely at once with an L2 evict_last hint (the k selected
-// positions are corrected later); the lane keeps the max |b| of the pass:
-// NP*32 group maxima of 16 positions.
-//
-// Selection (chunk i-1), stages:
-//  S. T = the largest key (bits 31..14) with >= k_eff group maxima >= T
-//     (bitwise search, warp reductions): >= k_eff elements have key >= T,
-//     typically ~1.2 k_eff.
-//  B. the groups whose max reaches T are spread over the lanes and their
-//     16 values re-read from e (an L2 hit); values with key >= T become
-//     candidates key<<16 | ~pos in warp smem.
-//  R. exact rank of each candidate by counting (ties: lower position first,
-//     R#3, R#4); rank < k_eff -> selected; bitmap prefix gives each its slot in
-//     ascending position (R#5).  More than CAP candidates (constant / zero /
-//     tied chunks) or a non-finite value: exact radix select over all
-//     positions (4 rounds of 8-bit digits).
-//  Q. 2-bit quantiser + record (R#1, R#6, R#13, R#14).
-//  F. EF residual of the selected positions, e = b - dequant.
-#include "chunk_io.cuh"
-#include "quant_pack.cuh"
+// CTAs of 8 independent warps, no block-level synchronisation.  Warp w walks
+// chunks w, w+W, ...: it streams the chunk in NP passes (all 12 128-bit loads
+// of a pass issued before any store), forms b = fma(beta, e, theta -
+// theta_local) (R#12), stores e <- b densely (L2 evict_last), keeps the 32*NP
+// group maxima, then runs the selection stages of warp_select.cuh.
+#include "warp_select.cuh"
 
 namespace slc {
 namespace {
 
+using namespace wsel;
+
 constexpr int kWarps = 8;  // warps per CTA
-#ifndef SLC_MINB
-#define SLC_MINB 2  // CTAs per SM the register budget is sized for
-#endif
-
-template <int C>
-struct WarpCfg {
-  static constexpr int NP = C / 512;       // passes of 16 positions per lane
-  static constexpr int B = (C == 1024) ? 32 : (C == 4096 ? 64 : 128);
-  static constexpr int RPQ_SHIFT = (B == 32) ? 3 : (B == 64 ? 4 : 5);  // log2(B/4)
-  static constexpr int BW = C / 32;         // bitmap words
-  static constexpr int CAP = 256;           // candidate capacity
-};
-
-// per-warp shared scratch
-template <int C>
-struct WarpScratch {
-  uint64_t cand[WarpCfg<C>::CAP];
-  float candb[WarpCfg<C>::CAP];
-  uint32_t bit[WarpCfg<C>::BW];
-  uint32_t wpre[WarpCfg<C>::BW];
-  uint32_t hist[256];  // fallback histogram; also the group list of stage B
-  uint32_t selpos[kMaxK];
-  float selval[kMaxK];
-  uint32_t code[kMaxK];
-};
-
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-__device__ __forceinline__ void st_f32x4_evict_last(float* ptr, float x, float y, float z, float w, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(x), "f"(y), "f"(z),
-               "f"(w), "l"(pol)
-               : "memory");
-}
-
-__device__ __forceinline__ float absmax_nan(float m, float x) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(m), "f"(fabsf(x)));
-  return r;
-}
-
-// element offset of the 4-position group q of chunk d
-template <int RPQ_SHIFT>
-__device__ __forceinline__ int64_t goff(const ChunkDesc& d, int q) {
-  return d.ld ? d.base + (int64_t)(q >> RPQ_SHIFT) * d.ld + 4 * (q & ((1 << RPQ_SHIFT) - 1)) : d.base + 4 * (int64_t)q;
-}
-
-template <int B>
-__device__ __forceinline__ int64_t pos_off(const ChunkDesc& d, int p) {
-  return d.ld ? d.base + (int64_t)(p / B) * d.ld + (p % B) : d.base + p;
-}
-
-// selection state of the chunk whose selection runs during the next chunk's stream
-struct Sel {
-  int64_t c;  // -1: none
-  ChunkDesc d;
-  int len, k_eff;
-  bool full, bad;
-  uint32_t Tc;
-  int M;  // candidates; > CAP: fallback
-  QuantOut q;
-};
+constexpr int kCap = 256;
 
 template <int C, bool BF16, int KC, int IBC>
-struct Compressor {
-  using K = WarpCfg<C>;
-  static constexpr int NP = K::NP;
-  const CompressArgs& a;
-  WarpScratch<C>& ws;
-  int lane;
-  int k;
-
-  // ---- S ---------------------------------------------------------------------------
-  __device__ __forceinline__ void stage_S(Sel& s, const uint32_t (&gk)[NP]) {
-    uint32_t gmaxk = 0;
-#pragma unroll
-    for (int u = 0; u < NP; u++) gmaxk = max(gmaxk, gk[u]);
-    s.bad = __reduce_max_sync(kFull, gmaxk) >= 0xFF000001u;  // |b| = inf or NaN somewhere
-    if (s.bad && lane == 0) atomicOr(a.err, kErrNonFinite);
-    uint32_t T = 0;
-#pragma unroll
-    for (int bit = 31; bit >= 14; --bit) {
-      const uint32_t Tp = T | (1u << bit);
-      int cnt = 0;
-#pragma unroll
-      for (int u = 0; u < NP; u++) cnt += gk[u] >= Tp;
-      if ((int)__reduce_add_sync(kFull, (unsigned)cnt) >= s.k_eff) T = Tp;
-    }
-    s.Tc = max(T, 1u);
-  }
-
-  // ---- B ---------------------------------------------------------------------------
-  __device__ __forceinline__ void stage_B(Sel& s, const uint32_t (&gk)[NP]) {
-    __syncwarp();  // e of chunk s.c (written by all lanes) is read back by other lanes
-    uint32_t gmask = 0;
-#pragma unroll
-    for (int u = 0; u < NP; u++) gmask |= (uint32_t)(gk[u] >= s.Tc) << u;
-    const int gcnt = __popc(gmask);
-    const int gbase = warp_excl_scan(gcnt);
-    const int G = (int)__reduce_add_sync(kFull, (unsigned)gcnt);
-    int M = 0;
-    if (!s.bad && G <= 256) {
-      {
-        int o = gbase;
-        uint32_t mm = gmask;
-        while (mm) {
-          const int u = __ffs(mm) - 1;
-          mm &= mm - 1;
-          ws.hist[o++] = (uint32_t)(lane * NP + u);
-        }
-      }
-      __syncwarp();
-      for (int r = 0; r < G; r += 32) {
-        const int gi = r + lane;
-        uint32_t cmask = 0;
-        int owner = 0, u = 0;
-        float vals[16];
-        if (gi < G) {
-          const uint32_t id = ws.hist[gi];
-          owner = (int)(id / NP);
-          u = (int)(id % NP);
-#pragma unroll
-          for (int v = 0; v < 4; v++) {
-            const int q = 128 * u + 32 * v + owner;
-            const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
-            load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, &vals[4 * v]);
-#pragma unroll
-            for (int j = 0; j < 4; j++)
-              if (j < nv && key2_of(vals[4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
-          }
-        }
-        const int cc = __popc(cmask);
-        int o = M + warp_excl_scan(cc);
-        M += (int)__reduce_add_sync(kFull, (unsigned)cc);
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          if ((cmask >> j) & 1u) {
-            const int p = 4 * (128 * u + 32 * (j >> 2) + owner) + (j & 3);
-            if (o < K::CAP) {
-              ws.cand[o] = ((uint64_t)key2_of(vals[j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
-              ws.candb[o] = vals[j];
-            }
-            o++;
-          }
-        }
-      }
-    } else {
-      M = K::CAP + 1;
-    }
-    s.M = M;
-    for (int w = lane; w < K::BW; w += 32) ws.bit[w] = 0u;
-    __syncwarp();
-  }
-
-  // ---- R: exact selection -> slots ---------------------------------------------------
-  __device__ __forceinline__ void bitmap_prefix() {
-    constexpr int WPL = K::BW / 32;
-    uint32_t w[WPL];
-    int cw = 0;
-#pragma unroll
-    for (int x = 0; x < WPL; x++) { w[x] = ws.bit[WPL * lane + x]; cw += __popc(w[x]); }
-    int pre = warp_excl_scan(cw);
-#pragma unroll
-    for (int x = 0; x < WPL; x++) { ws.wpre[WPL * lane + x] = (uint32_t)pre; pre += __popc(w[x]); }
-  }
-
-  __device__ __forceinline__ void stage_R(const Sel& s) {
-    const int M = s.M;
-    if (M <= K::CAP) {
-      // lane owns candidates lane + 32m; each broadcast candidate is compared with the owned ones
-      const int NM = (M + 31) >> 5;
-      constexpr int MM = K::CAP / 32;
-      uint64_t mine[MM];
-      int rank[MM];
-#pragma unroll
-      for (int m = 0; m < MM; m++) {
-        mine[m] = (lane + 32 * m < M) ? ws.cand[lane + 32 * m] : ~0ull;
-        rank[m] = 0;
-      }
-      if (NM <= 3) {
-#pragma unroll 4
-        for (int j = 0; j < M; j++) {
-          const uint64_t x = ws.cand[j];
-          rank[0] += x > mine[0];
-          rank[1] += x > mine[1];
-          rank[2] += x > mine[2];
-        }
-      } else {
-        for (int j = 0; j < M; j++) {
-          const uint64_t x = ws.cand[j];
-#pragma unroll
-          for (int m = 0; m < MM; m++) rank[m] += x > mine[m];
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < MM; m++) {
-        if (lane + 32 * m < M && rank[m] < s.k_eff) {
-          const uint32_t p = 0xFFFFu - (uint32_t)(mine[m] & 0xFFFFu);
-          atomicOr(&ws.bit[p >> 5], 1u << (p & 31));
-        }
-      }
-      __syncwarp();
-      bitmap_prefix();
-      __syncwarp();
-#pragma unroll
-      for (int m = 0; m < MM; m++) {
-        const int ci = lane + 32 * m;
-        if (ci < M && rank[m] < s.k_eff) {
-          const uint32_t p = 0xFFFFu - (uint32_t)(mine[m] & 0xFFFFu);
-          const int sl = (int)ws.wpre[p >> 5] + __popc(ws.bit[p >> 5] & ((1u << (p & 31)) - 1u));
-          ws.selpos[sl] = p;
-          ws.selval[sl] = ws.candb[ci];
-        }
-      }
-    } else {
-      fallback(s);
-    }
-    __syncwarp();
-  }
-
-  // exact k_eff-th largest key by 4 rounds of 8-bit radix select over all positions,
-  // then key > K plus the first `need` positions with key == K (lower position wins)
-  __device__ __noinline__ void fallback(const Sel& s) {
-    uint32_t Kth = 0;
-    int need = s.k_eff;
-#pragma unroll 1
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = lane; i < 256; i += 32) ws.hist[i] = 0u;
-      __syncwarp();
-      const uint32_t hi_mask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-#pragma unroll 1
-      for (int u = 0; u < NP; u++) {
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-          const int q = 128 * u + 32 * v + lane;
-          const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
-          float ev[4];
-          load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, ev);
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const uint32_t key = key2_of(ev[j]);
-            if (j < nv && (key & hi_mask) == (Kth & hi_mask)) atomicAdd(&ws.hist[(key >> shift) & 255u], 1u);
-          }
-        }
-      }
-      __syncwarp();
-      // digit D: #(digit > D) < need <= #(digit >= D); lane l holds bins 8l..8l+7
-      uint32_t h[8];
-      uint32_t s8 = 0;
-#pragma unroll
-      for (int x = 0; x < 8; x++) { h[x] = ws.hist[8 * lane + x]; s8 += h[x]; }
-      uint32_t inc = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_down_sync(kFull, inc, o);
-        if (lane + o < 32) inc += y;
-      }
-      uint32_t acc = inc - s8;  // bins in lanes above
-      int found = -1;
-      uint32_t found_gt = 0;
-#pragma unroll
-      for (int x = 7; x >= 0; x--) {
-        if (found < 0 && acc < (uint32_t)need && acc + h[x] >= (uint32_t)need) { found = 8 * lane + x; found_gt = acc; }
-        acc += h[x];
-      }
-      const int src = __ffs(__ballot_sync(kFull, found >= 0)) - 1;
-      Kth |= (uint32_t)__shfl_sync(kFull, found, src) << shift;
-      need -= (int)__shfl_sync(kFull, found_gt, src);
-      __syncwarp();
-    }
-    int taken = 0;
-#pragma unroll 1
-    for (int u = 0; u < NP; u++) {
-#pragma unroll
-      for (int v = 0; v < 4; v++) {
-        // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
-        const int q = 128 * u + 32 * v + lane;
-        const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
-        float ev[4];
-        load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, ev);
-        uint32_t tmask = 0;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const uint32_t key = key2_of(ev[j]);
-          if (j < nv && key > Kth) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
-          if (j < nv && key == Kth) tmask |= 1u << j;
-        }
-        const int tc = __popc(tmask);
-        int o = taken + warp_excl_scan(tc);
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          if ((tmask >> j) & 1u) {
-            if (o < need) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
-            o++;
-          }
-        }
-        taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
-      }
-    }
-    __syncwarp();
-    // slots in ascending position; values re-read from e (= b, written by the stream)
-    constexpr int WPL = K::BW / 32;
-    uint32_t w[WPL];
-    int cw = 0;
-#pragma unroll
-    for (int x = 0; x < WPL; x++) { w[x] = ws.bit[WPL * lane + x]; cw += __popc(w[x]); }
-    int pre = warp_excl_scan(cw);
-#pragma unroll
-    for (int x = 0; x < WPL; x++) {
-      uint32_t y = w[x];
-      while (y) {
-        const int bp = __ffs(y) - 1;
-        y &= y - 1;
-        const int p = 32 * (WPL * lane + x) + bp;
-        if (pre < kMaxK) {
-          ws.selpos[pre] = (uint32_t)p;
-          ws.selval[pre] = a.ef[pos_off<K::B>(s.d, p)];
-        }
-        pre++;
-      }
-    }
-  }
-
-  // ---- Q, F ----------------------------------------------------------------------------
-  __device__ __forceinline__ void stage_Q(Sel& s) {
-    s.q = warp_quantize_pack<KC, IBC>(ws.selpos, ws.selval, ws.code, k, s.k_eff, a.g,
-                                      a.records + s.c * a.g.rec_words, a.err);
-  }
-
-  __device__ __forceinline__ void stage_F(const Sel& s) {
-    for (int j = lane; j < s.k_eff; j += 32) {
-      const int p = (int)ws.selpos[j];
-      const float bb = ws.selval[j];
-      const float mag = fabsf(bb) > s.q.tau ? s.q.fhi : s.q.flo;
-      a.ef[pos_off<K::B>(s.d, p)] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
-    }
-    __syncwarp();
-  }
-
-  // selection work scheduled at pass u (NP >= 5: one stage per pass; fewer passes merge stages)
-  __device__ __forceinline__ void stages_at(int u, Sel& s, const uint32_t (&gk)[NP]) {
-    if (s.c < 0) return;
-    if (u == 0) stage_S(s, gk);
-    if (u == (NP > 1 ? 1 : 0)) stage_B(s, gk);
-    if (u == (NP > 2 ? 2 : NP - 1)) stage_R(s);
-    if (u == (NP > 3 ? 3 : NP - 1)) stage_Q(s);
-    if (u == (NP > 4 ? 4 : NP - 1)) stage_F(s);
-  }
-};
-
-template <int C, bool BF16, int KC, int IBC>
-__global__ void __launch_bounds__(kWarps * 32, SLC_MINB) compress_warp_kernel(const CompressArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 2) compress_warp_kernel(const CompressArgs a) {
   using K = WarpCfg<C>;
   constexpr int NP = K::NP;
+  using Scratch = WarpScratch<C, kCap, kMaxK>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Compressor<C, BF16, KC, IBC> cp{a, reinterpret_cast<WarpScratch<C>*>(smem_raw)[warp], lane, KC ? KC : a.g.k};
+  Compressor<C, BF16, KC, IBC, kCap, kMaxK> cp{a, reinterpret_cast<Scratch*>(smem_raw)[warp], lane,
+                                                KC ? KC : a.g.k};
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const uint64_t pol_last = l2_policy_evict_last();
 
-  Sel sel;
-  sel.c = -1;
-  uint32_t sgk[NP];  // group maxima of the chunk being selected
-#pragma unroll
-  for (int u = 0; u < NP; u++) sgk[u] = 0;
-
-  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp;; c += W) {
-    const bool have = c < a.n_chunks;
-    if (!have && sel.c < 0) break;
-    ChunkDesc d;
-    d.base = 0; d.ld = 0; d.len = C;
-    if (have) d = a.chunks[c];
-    const int len = d.len;
-    const bool full = len == C;
+  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < a.n_chunks; c += W) {
+    Sel s;
+    s.c = c;
+    s.d = a.chunks[c];
+    s.len = s.d.len;
+    s.full = s.len == C;
+    s.k_eff = s.full ? cp.k : max(1, (cp.k * s.len) / C);
+    const ChunkDesc& d = s.d;
     uint32_t gk[NP];
-
 #pragma unroll
     for (int u = 0; u < NP; u++) {
-      // 1. issue every load of pass u (12 x 128-bit per lane) before any store
       float av[16], lv[16], ev[16];
-      if (have) {
-        if (full) {
 #pragma unroll
-          for (int v = 0; v < 4; v++) {
-            const int64_t off = goff<K::RPQ_SHIFT>(d, 128 * u + 32 * v + lane);
-            load_param4<BF16>(a.theta, off, 4, &av[4 * v]);
-            load_param4<BF16>(a.theta_local, off, 4, &lv[4 * v]);
-            load_f32x4(a.ef, off, 4, &ev[4 * v]);
-          }
+      for (int v = 0; v < 4; v++) {
+        const int q = 128 * u + 32 * v + lane;
+        const int64_t off = goff<K::RPQ_SHIFT>(d, q);
+        const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
+        load_param4<BF16>(a.theta, off, nv, &av[4 * v]);
+        load_param4<BF16>(a.theta_local, off, nv, &lv[4 * v]);
+        load_f32x4(a.ef, off, nv, &ev[4 * v]);
+      }
+      float gm = 0.0f;
+#pragma unroll
+      for (int x = 0; x < 16; x++) {
+        av[x] = __fmaf_rn(a.beta, ev[x], __fsub_rn(av[x], lv[x]));  // b
+        gm = absmax_nan(gm, av[x]);  // missing positions hold b = 0: never above a valid max
+      }
+      int nvalid = 16;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int q = 128 * u + 32 * v + lane;
+        const int64_t off = goff<K::RPQ_SHIFT>(d, q);
+        if (s.full) {
+          st_f32x4_evict_last(a.ef + off, av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3], pol_last);
         } else {
-#pragma unroll
-          for (int v = 0; v < 4; v++) {
-            const int q = 128 * u + 32 * v + lane;
-            const int64_t off = goff<K::RPQ_SHIFT>(d, q);
-            const int nv = valid_in_group(4 * q, len);
-            load_param4<BF16>(a.theta, off, nv, &av[4 * v]);
-            load_param4<BF16>(a.theta_local, off, nv, &lv[4 * v]);
-            load_f32x4(a.ef, off, nv, &ev[4 * v]);
-          }
+          const int nv = valid_in_group(4 * q, s.len);
+          nvalid -= 4 - nv;
+          store_f32x4(a.ef, off, nv, &av[4 * v]);
         }
       }
-      // 2. meanwhile: a stage of the previous chunk's selection
-      cp.stages_at(u, sel, sgk);
-      // 3. consume: b, dense e <- b, group maximum
-      if (have) {
-        float gm = 0.0f;
-#pragma unroll
-        for (int x = 0; x < 16; x++) {
-          av[x] = __fmaf_rn(a.beta, ev[x], __fsub_rn(av[x], lv[x]));  // b
-          gm = absmax_nan(gm, av[x]);  // missing positions hold b = 0: never above a valid max
-        }
-        int nvalid = 16;
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-          const int q = 128 * u + 32 * v + lane;
-          const int64_t off = goff<K::RPQ_SHIFT>(d, q);
-          if (full) {
-            st_f32x4_evict_last(a.ef + off, av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3], pol_last);
-          } else {
-            const int nv = valid_in_group(4 * q, len);
-            nvalid -= 4 - nv;
-            store_f32x4(a.ef, off, nv, &av[4 * v]);
-          }
-        }
-        gk[u] = nvalid ? key2_of(gm) : 0u;
-      }
+      gk[u] = nvalid ? key2_of(gm) : 0u;
     }
-    // the chunk just streamed is selected during the next iteration
-    if (have) {
-      sel.c = c;
-      sel.d = d;
-      sel.len = len;
-      sel.full = full;
-      sel.k_eff = full ? cp.k : max(1, (cp.k * len) / C);
-#pragma unroll
-      for (int u = 0; u < NP; u++) sgk[u] = gk[u];
-    } else {
-      sel.c = -1;
-    }
+    cp.select(s, gk);
   }
 }
 
 template <int C, bool BF16, int KC, int IBC>
 cudaError_t launch_warp_t(const CompressArgs& a, cudaStream_t s) {
-  constexpr size_t smem = sizeof(WarpScratch<C>) * kWarps;
+  constexpr size_t smem = sizeof(WarpScratch<C, kCap, kMaxK>) * kWarps;
   auto kern = compress_warp_kernel<C, BF16, KC, IBC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -1,6 +1,8 @@
 // plan.cpp — host side of libslc: geometry validation, FSDP-style shard
 // partition (R#11), per-chunk table, payload-header checks, error
 // latch and the C-ABI entry points declared in include/slc.h.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,6 +25,12 @@ struct slc_plan {
   int64_t total_elems = 0, total_chunks = 0, first_chunk = 0, n_chunks = 0, shard_elems = 0;
   ChunkDesc* d_chunks = nullptr;
   uint32_t* d_err = nullptr;
+  // TMA: one (theta, theta_local, e) tensor-map triple per blocked segment,
+  // encoded for the buffers of the last slc_compress call
+  std::vector<int> blk_segs;  // index into segs
+  std::vector<CUtensorMap> h_tmaps;
+  CUtensorMap* d_tmaps = nullptr;
+  const void* tmap_ptrs[3] = {nullptr, nullptr, nullptr};
   slc_status latched = SLC_OK;
   uint8_t digest[32];
 };
@@ -174,6 +182,53 @@ slc_status cuda_status(cudaError_t e, slc_plan* p) {
 
 bool aligned16(const void* q) { return (((uintptr_t)q) & 15u) == 0; }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// (re)encode the 64x64-box tensor maps of every blocked segment for these buffers
+cudaError_t ensure_tmaps(slc_plan* p, const void* theta, const void* theta_local, const float* ef,
+                         cudaStream_t stream) {
+  if (p->blk_segs.empty()) return cudaSuccess;
+  if (p->tmap_ptrs[0] == theta && p->tmap_ptrs[1] == theta_local && p->tmap_ptrs[2] == ef) return cudaSuccess;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const int B = p->geom.block;
+  const int pb = p->dtype == SLC_BF16 ? 2 : 4;
+  const void* bufs[3] = {theta, theta_local, ef};
+  for (size_t i = 0; i < p->blk_segs.size(); i++) {
+    const slc_segment& s = p->segs[p->blk_segs[i]];
+    for (int a = 0; a < 3; a++) {
+      const int esz = a < 2 ? pb : 4;
+      const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+      char* base = (char*)bufs[a] + (size_t)s.shard_offset * esz;
+      const cuuint64_t dims[2] = {(cuuint64_t)s.cols, (cuuint64_t)s.rows};
+      const cuuint64_t strides[1] = {(cuuint64_t)s.cols * esz};
+      const cuuint32_t box[2] = {(cuuint32_t)B, (cuuint32_t)B};
+      const cuuint32_t estr[2] = {1, 1};
+      CUresult r = enc(&p->h_tmaps[3 * i + a], dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(p->d_tmaps, p->h_tmaps.data(), p->h_tmaps.size() * sizeof(CUtensorMap),
+                                  cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  p->tmap_ptrs[0] = theta;
+  p->tmap_ptrs[1] = theta_local;
+  p->tmap_ptrs[2] = ef;
+  return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -249,7 +304,8 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
         s.n_chunks = (s.rows / B) * nb;
         for (int64_t bi = 0; bi < s.rows / B; bi++)
           for (int64_t bj = 0; bj < nb; bj++)
-            table.push_back(ChunkDesc{s.shard_offset + bi * B * cols + bj * B, (int32_t)cols, (int32_t)C});
+            table.push_back(ChunkDesc{s.shard_offset + bi * B * cols + bj * B, (int32_t)cols, (int32_t)C,
+                                      (int32_t)p->blk_segs.size(), (int32_t)(bj * B), (int32_t)(bi * B), 0});
       } else {
         s.rows = s.n_elems;
         s.cols = 1;
@@ -258,11 +314,12 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
         s.n_chunks = (s.n_elems + C - 1) / C;
         for (int64_t c = 0; c < s.n_chunks; c++) {
           const int64_t len = std::min(C, s.n_elems - c * C);
-          table.push_back(ChunkDesc{s.shard_offset + c * C, 0, (int32_t)len});
+          table.push_back(ChunkDesc{s.shard_offset + c * C, 0, (int32_t)len, -1, 0, 0, 0});
         }
       }
       if (!first_set) { p->first_chunk = s.first_chunk; first_set = true; }
       shard_off = s.shard_offset + s.n_elems;
+      if (s.blocked) p->blk_segs.push_back((int)p->segs.size());
       p->segs.push_back(s);
     }
     off += n;
@@ -287,6 +344,10 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
   DeviceGuard guard(device);
   cudaError_t ce = cudaMalloc(&p->d_err, sizeof(uint32_t));
   if (ce == cudaSuccess) ce = cudaMemset(p->d_err, 0, sizeof(uint32_t));
+  if (ce == cudaSuccess && !p->blk_segs.empty()) {
+    p->h_tmaps.resize(3 * p->blk_segs.size());
+    ce = cudaMalloc(&p->d_tmaps, p->h_tmaps.size() * sizeof(CUtensorMap));
+  }
   if (ce == cudaSuccess && !table.empty()) {
     ce = cudaMalloc(&p->d_chunks, table.size() * sizeof(ChunkDesc));
     if (ce == cudaSuccess)
@@ -295,6 +356,7 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
   if (ce != cudaSuccess) {
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_chunks) cudaFree(p->d_chunks);
+    if (p->d_tmaps) cudaFree(p->d_tmaps);
     delete p;
     cudaGetLastError();
     return SLC_ERR_CUDA;
@@ -332,6 +394,7 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   if (!aligned16(theta) || !aligned16(theta_local) || !aligned16(ef) || (((uintptr_t)records) & 3u))
     return SLC_ERR_INVALID_ARGUMENT;
   slc::CompressArgs a;
+  a.tmaps = p->d_tmaps;
   a.chunks = p->d_chunks;
   a.n_chunks = p->n_chunks;
   a.theta = theta;
@@ -342,7 +405,13 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   a.beta = beta;
   a.g = p->g;
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_compress(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (slc::compress_tma_supported(p->g)) {
+    cudaError_t e = ensure_tmaps(p, theta, theta_local, ef, st);
+    if (e != cudaSuccess) return cuda_status(e, p);
+    return cuda_status(slc::launch_compress_tma(a, p->dtype == SLC_BF16, st), p);
+  }
+  return cuda_status(slc::launch_compress(a, p->dtype == SLC_BF16, st), p);
 }
 
 slc_status slc_decode_aggregate(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
@@ -407,6 +476,7 @@ void slc_plan_destroy(slc_plan* p) {
     DeviceGuard guard(p->device);
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_err) cudaFree(p->d_err);
+    if (p->d_tmaps) cudaFree(p->d_tmaps);
   }
   delete p;
 }

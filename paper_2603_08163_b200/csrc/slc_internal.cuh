@@ -16,12 +16,17 @@ constexpr int kMaxK = 256;
 //   base + (p / B) * ld + (p % B)   (blocked, ld = tensor cols)
 //   base + p                        (flat,    ld = 0)
 // len = number of positions (C, or less for the last chunk of a flat tensor).
+// Blocked chunks also carry their TMA coordinates: tensor map triple `tmap`
+// (theta, theta_local, e of the chunk's segment) and the block's (col, row).
 struct __align__(16) ChunkDesc {
   int64_t base;
   int32_t ld;
   int32_t len;
+  int32_t tmap;  // -1: flat chunk
+  int32_t tx, ty;
+  int32_t pad;
 };
-static_assert(sizeof(ChunkDesc) == 16, "ChunkDesc must be 16 bytes");
+static_assert(sizeof(ChunkDesc) == 32, "ChunkDesc must be 32 bytes");
 
 // Error bits latched on the device.
 enum : uint32_t { kErrNonFinite = 1u, kErrScaleOverflow = 2u };
@@ -32,6 +37,7 @@ struct Geom {
 };
 
 struct CompressArgs {
+  const void* tmaps;  // CUtensorMap[3 * blocked segments] (theta, theta_local, e), device memory
   const ChunkDesc* chunks;
   int64_t n_chunks;
   const void* theta;
@@ -67,6 +73,9 @@ cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t 
 cudaError_t launch_compress_simple(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one warp per chunk, no block-level synchronisation (C = 1024, 4096)
 cudaError_t launch_compress_warp(const CompressArgs& a, int param_bf16, cudaStream_t s);
+// TMA producer warp + warp-per-chunk consumers (C = 4096, k = 64, 12-bit indices)
+cudaError_t launch_compress_tma(const CompressArgs& a, int param_bf16, cudaStream_t s);
+bool compress_tma_supported(const Geom& g);
 cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
 bool compress_supported(int C);
 
