@@ -31,6 +31,7 @@ WORKLOADS = {
     "llama2-7b": ("llama2-7b", 20, "f32"),         # BASELINE configs[4] base point
     "1m": ("1m-2d", 1, "f32"),                     # BASELINE configs[0]
     "flat-1b": ("flat-1b", 8, "f32"),              # bandwidth probe (contiguous chunks)
+    "tiny": ("llama-tiny", 4, "f32"),              # debugging
 }
 
 BETA = 0.95

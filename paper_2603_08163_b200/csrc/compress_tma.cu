@@ -45,7 +45,8 @@ struct TmaCfg {
   using Scratch = WarpScratch<kC, kCapT, kKmaxT>;
   static constexpr size_t off_scratch = S * stage_bytes;
   static constexpr size_t off_bar = off_scratch + kNC * sizeof(Scratch);
-  static constexpr size_t bytes = off_bar + 2 * S * sizeof(uint64_t);
+  static constexpr size_t off_rel = off_bar + 2 * S * sizeof(uint64_t);
+  static constexpr size_t bytes = off_rel + S * sizeof(int);
 };
 
 __device__ __forceinline__ void tma_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
@@ -64,6 +65,11 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::off_bar);
   uint64_t* empty = full + S;
+  // releases per stage so far: an mbarrier parity wait is only valid within one
+  // phase, and with NC > S consumers a consumer could otherwise start waiting
+  // on a stage several uses ahead — it first waits until the stage's previous
+  // use has been released
+  volatile int* rel = reinterpret_cast<volatile int*>(smem + T::off_rel);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t G = gridDim.x, n = a.n_chunks;
 
@@ -71,6 +77,7 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
     for (int s = 0; s < S; s++) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      rel[s] = 0;
     }
     ptx::fence_mbar_init();
   }
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
   // ======================= consumers =======================
   const int cw = warp - 1;
   auto& scratch = reinterpret_cast<typename T::Scratch*>(smem + T::off_scratch)[cw];
-  Compressor<kC, BF16, 64, 12, kCapT, kKmaxT> cp{a, scratch, lane, 64};
+  Compressor<kC, BF16, 64, 12, kCapT, kKmaxT> cp(a, scratch, lane, 64);
   const uint64_t pol_last = l2_policy_evict_last();
 
   for (int64_t i = cw;; i += kNC) {
@@ -126,7 +133,9 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
     sel.k_eff = sel.full ? 64 : max(1, (64 * sel.len) / kC);
     const ChunkDesc& d = sel.d;
     const unsigned char* st = smem + s * T::stage_bytes;
-    ptx::mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+    const int use = (int)(i / S);
+    while (rel[s] < use) __nanosleep(64);
+    ptx::mbar_wait(&full[s], (uint32_t)(use & 1));
 
     uint32_t gk[NP];
 #pragma unroll
@@ -182,7 +191,10 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
       gk[u] = nvalid ? key2_of(gm) : 0u;
     }
     __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[s]);  // stage read: the producer may refill it
+    if (lane == 0) {  // stage read: the producer may refill it
+      ptx::mbar_arrive(&empty[s]);
+      atomicAdd((int*)&rel[s], 1);
+    }
     cp.select(sel, gk);
   }
 }

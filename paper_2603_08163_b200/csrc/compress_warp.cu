@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) compress_warp_kernel(const Com
   using Scratch = WarpScratch<C, kCap, kMaxK>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Compressor<C, BF16, KC, IBC, kCap, kMaxK> cp{a, reinterpret_cast<Scratch*>(smem_raw)[warp], lane,
-                                                KC ? KC : a.g.k};
+  Compressor<C, BF16, KC, IBC, kCap, kMaxK> cp(a, reinterpret_cast<Scratch*>(smem_raw)[warp], lane,
+                                                KC ? KC : a.g.k);
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const uint64_t pol_last = l2_policy_evict_last();
 

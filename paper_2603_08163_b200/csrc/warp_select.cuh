@@ -94,10 +94,18 @@ template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
 struct Compressor {
   using K = WarpCfg<C>;
   static constexpr int NP = K::NP;
-  const CompressArgs& a;
+  // fields of CompressArgs held by value (a reference to the kernel's param
+  // struct would force the struct into local memory)
+  float* ef;
+  uint32_t* records;
+  uint32_t* err;
+  Geom g;
   WarpScratch<C, CAP, KMAX>& ws;
   int lane;
   int k;
+
+  __device__ __forceinline__ Compressor(const CompressArgs& a, WarpScratch<C, CAP, KMAX>& ws_, int lane_, int k_)
+      : ef(ef), records(records), err(err), g(a.g), ws(ws_), lane(lane_), k(k_) {}
 
   // ---- S ---------------------------------------------------------------------------
   __device__ __forceinline__ void stage_S(Sel& s, const uint32_t (&gk)[NP]) {
@@ -105,7 +113,7 @@ struct Compressor {
 #pragma unroll
     for (int u = 0; u < NP; u++) gmaxk = max(gmaxk, gk[u]);
     s.bad = __reduce_max_sync(kFull, gmaxk) >= 0xFF000001u;  // |b| = inf or NaN somewhere
-    if (s.bad && lane == 0) atomicOr(a.err, kErrNonFinite);
+    if (s.bad && lane == 0) atomicOr(err, kErrNonFinite);
     uint32_t T = 0;
 #pragma unroll
     for (int bit = 31; bit >= 14; --bit) {
@@ -152,7 +160,7 @@ struct Compressor {
           for (int v = 0; v < 4; v++) {
             const int q = 128 * u + 32 * v + owner;
             const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
-            load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, &vals[4 * v]);
+            load_f32x4(ef, goff<K::RPQ_SHIFT>(s.d, q), nv, &vals[4 * v]);
 #pragma unroll
             for (int j = 0; j < 4; j++)
               if (j < nv && key2_of(vals[4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
@@ -242,16 +250,16 @@ struct Compressor {
         }
       }
     } else {
-      fallback(s);
+      fallback(s.d, s.len, s.full, s.k_eff);
     }
     __syncwarp();
   }
 
   // exact k_eff-th largest key by 4 rounds of 8-bit radix select over all positions,
   // then key > K plus the first `need` positions with key == K (lower position wins)
-  __device__ __noinline__ void fallback(const Sel& s) {
+  __device__ __noinline__ void fallback(const ChunkDesc d, const int len, const bool full, const int k_eff) {
     uint32_t Kth = 0;
-    int need = s.k_eff;
+    int need = k_eff;
 #pragma unroll 1
     for (int shift = 24; shift >= 0; shift -= 8) {
       for (int i = lane; i < 256; i += 32) ws.hist[i] = 0u;
@@ -262,9 +270,9 @@ struct Compressor {
 #pragma unroll
         for (int v = 0; v < 4; v++) {
           const int q = 128 * u + 32 * v + lane;
-          const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
+          const int nv = full ? 4 : valid_in_group(4 * q, len);
           float ev[4];
-          load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, ev);
+          load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const uint32_t key = key2_of(ev[j]);
@@ -304,9 +312,9 @@ struct Compressor {
       for (int v = 0; v < 4; v++) {
         // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
         const int q = 128 * u + 32 * v + lane;
-        const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
+        const int nv = full ? 4 : valid_in_group(4 * q, len);
         float ev[4];
-        load_f32x4(a.ef, goff<K::RPQ_SHIFT>(s.d, q), nv, ev);
+        load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
         uint32_t tmask = 0;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
@@ -343,7 +351,7 @@ struct Compressor {
         const int p = 32 * (WPL * lane + x) + bp;
         if (pre < KMAX) {
           ws.selpos[pre] = (uint32_t)p;
-          ws.selval[pre] = a.ef[pos_off<K::B>(s.d, p)];
+          ws.selval[pre] = ef[pos_off<K::B>(d, p)];
         }
         pre++;
       }
@@ -352,8 +360,8 @@ struct Compressor {
 
   // ---- Q, F ----------------------------------------------------------------------------
   __device__ __forceinline__ void stage_Q(Sel& s) {
-    s.q = warp_quantize_pack<KC, IBC>(ws.selpos, ws.selval, ws.code, k, s.k_eff, a.g,
-                                      a.records + s.c * a.g.rec_words, a.err);
+    s.q = warp_quantize_pack<KC, IBC>(ws.selpos, ws.selval, ws.code, k, s.k_eff, g,
+                                      records + s.c * g.rec_words, err);
   }
 
   __device__ __forceinline__ void stage_F(const Sel& s) {
@@ -361,7 +369,7 @@ struct Compressor {
       const int p = (int)ws.selpos[j];
       const float bb = ws.selval[j];
       const float mag = fabsf(bb) > s.q.tau ? s.q.fhi : s.q.flo;
-      a.ef[pos_off<K::B>(s.d, p)] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
+      ef[pos_off<K::B>(s.d, p)] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
     }
     __syncwarp();
   }

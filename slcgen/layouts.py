@@ -83,6 +83,8 @@ LAYOUTS = {
     # configs[4]: 7B sweep (Llama-2-7B shapes)
     "llama2-7b": llama(d=4096, L=32, n_heads=32, n_kv=32, F=11008, V=32000, tied=False),
     "ragged": RAGGED,
+    # small Llama for multi-chunk-per-CTA tests (~12M params, ~3k chunks incl. partial norms)
+    "llama-tiny": llama(d=512, L=2, n_heads=8, n_kv=2, F=1536, V=16384, tied=False),
     # bandwidth probes: the 1B parameter count as one flat tensor / as 64-row-blocked matrices
     "flat-1b": [("w", (1235814400,))],
 }
