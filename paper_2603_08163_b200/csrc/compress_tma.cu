@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
       if (use > 0) ptx::mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
       const ChunkDesc d = a.chunks[c];
       unsigned char* st = smem + s * T::stage_bytes;
+      SLC_CHECK(d.tmap < 0 || 3 * d.tmap + 2 < a.n_tmaps, "producer tmap index");
+      SLC_CHECK(d.base >= 0 && d.base + (d.ld ? 63LL * d.ld + 64 : (int64_t)d.len) <= a.n_elems, "producer chunk range");
       if (d.len != kC) {
         ptx::mbar_arrive(&full[s]);  // partial chunk: read from global by the consumer
       } else {
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
     const int use = (int)(i / S);
     while (rel[s] < use) __nanosleep(64);
     ptx::mbar_wait(&full[s], (uint32_t)(use & 1));
+    SLC_CHECK(d.base >= 0 && d.base + (d.ld ? 63LL * d.ld + 64 : (int64_t)d.len) <= a.n_elems, "consumer chunk range");
 
     uint32_t gk[NP];
 #pragma unroll
@@ -181,7 +184,9 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
         const int q = 128 * u + 32 * v + lane;
         const int64_t off = goff<4>(d, q);
         if (sel.full) {
+#ifndef SLC_DBG_NOSTORE
           st_f32x4_evict_last(a.ef + off, av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3], pol_last);
+#endif
         } else {
           const int nv = valid_in_group(4 * q, sel.len);
           nvalid -= 4 - nv;
@@ -195,7 +200,14 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
       ptx::mbar_arrive(&empty[s]);
       atomicAdd((int*)&rel[s], 1);
     }
+#ifdef SLC_DBG_B
+    if (lane == 0 && c < 2)
+      printf("consumer chunk %lld a.ef=%p a.records=%p a.n_elems=%lld cp.ef=%p cp.n_elems=%lld\n", (long long)c,
+             (void*)a.ef, (void*)a.records, (long long)a.n_elems, (void*)cp.ef, (long long)cp.n_elems);
+#endif
+#ifndef SLC_DBG_NOSELECT
     cp.select(sel, gk);
+#endif
   }
 }
 

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -177,6 +179,7 @@ slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const*
 slc_status cuda_status(cudaError_t e, slc_plan* p) {
   if (e == cudaSuccess) return SLC_OK;
   p->latched = SLC_ERR_CUDA;
+  if (std::getenv("SLC_DEBUG")) std::fprintf(stderr, "libslc: CUDA error %d: %s\n", (int)e, cudaGetErrorString(e));
   return SLC_ERR_CUDA;
 }
 
@@ -394,6 +397,8 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   if (!aligned16(theta) || !aligned16(theta_local) || !aligned16(ef) || (((uintptr_t)records) & 3u))
     return SLC_ERR_INVALID_ARGUMENT;
   slc::CompressArgs a;
+  a.n_elems = p->shard_elems;
+  a.n_tmaps = (int32_t)p->h_tmaps.size();
   a.tmaps = p->d_tmaps;
   a.chunks = p->d_chunks;
   a.n_chunks = p->n_chunks;

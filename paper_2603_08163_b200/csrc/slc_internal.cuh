@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <vector>
 
@@ -36,7 +37,24 @@ struct Geom {
   int idx_words, code_words, rec_words;
 };
 
+#ifdef SLC_CHECKED  // debug builds: bounds-checked kernels
+#define SLC_CHECK(cond, what)                                                                          \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("SLC_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                             \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define SLC_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 struct CompressArgs {
+  int64_t n_elems;    // shard buffer length (bounds checks in debug builds)
+  int32_t n_tmaps;
   const void* tmaps;  // CUtensorMap[3 * blocked segments] (theta, theta_local, e), device memory
   const ChunkDesc* chunks;
   int64_t n_chunks;

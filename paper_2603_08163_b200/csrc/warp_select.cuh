@@ -100,12 +100,21 @@ struct Compressor {
   uint32_t* records;
   uint32_t* err;
   Geom g;
+  int64_t n_elems, n_chunks;
   WarpScratch<C, CAP, KMAX>& ws;
   int lane;
   int k;
 
   __device__ __forceinline__ Compressor(const CompressArgs& a, WarpScratch<C, CAP, KMAX>& ws_, int lane_, int k_)
-      : ef(ef), records(records), err(err), g(a.g), ws(ws_), lane(lane_), k(k_) {}
+      : ef(a.ef),
+        records(a.records),
+        err(a.err),
+        g(a.g),
+        n_elems(a.n_elems),
+        n_chunks(a.n_chunks),
+        ws(ws_),
+        lane(lane_),
+        k(k_) {}
 
   // ---- S ---------------------------------------------------------------------------
   __device__ __forceinline__ void stage_S(Sel& s, const uint32_t (&gk)[NP]) {
@@ -128,6 +137,12 @@ struct Compressor {
 
   // ---- B ---------------------------------------------------------------------------
   __device__ __forceinline__ void stage_B(Sel& s, const uint32_t (&gk)[NP]) {
+#ifdef SLC_DBG_B
+    if (lane == 0 && s.c < 2)
+      printf("stage_B chunk %lld ef=%p records=%p err=%p n_elems=%lld n_chunks=%lld k=%d lane=%d ws=%p\n",
+             (long long)s.c, (void*)ef, (void*)records, (void*)err, (long long)n_elems, (long long)n_chunks, k, lane,
+             (void*)&ws);
+#endif
     __syncwarp();  // e of chunk s.c (written by all lanes) is read back by other lanes
     uint32_t gmask = 0;
 #pragma unroll
@@ -156,10 +171,22 @@ struct Compressor {
           const uint32_t id = ws.hist[gi];
           owner = (int)(id / NP);
           u = (int)(id % NP);
+          SLC_CHECK(owner < 32 && u < NP, "stage_B group id");
 #pragma unroll
           for (int v = 0; v < 4; v++) {
             const int q = 128 * u + 32 * v + owner;
             const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
+#ifdef SLC_DBG_B
+            {
+              const int64_t o = goff<K::RPQ_SHIFT>(s.d, q);
+              if (o < 0 || o + 4 > n_elems) {
+                printf("stage_B bad offset %lld chunk %lld owner %d u %d gi %d G %d base %lld ld %d len %d\n",
+                       (long long)o, (long long)s.c, owner, u, gi, G, (long long)s.d.base, s.d.ld, s.d.len);
+                for (int j = 0; j < 4; j++) vals[4 * v + j] = 0.0f;
+                continue;
+              }
+            }
+#endif
             load_f32x4(ef, goff<K::RPQ_SHIFT>(s.d, q), nv, &vals[4 * v]);
 #pragma unroll
             for (int j = 0; j < 4; j++)
@@ -245,6 +272,7 @@ struct Compressor {
         if (ci < M && rank[m] < s.k_eff) {
           const uint32_t p = 0xFFFFu - (uint32_t)(mine[m] & 0xFFFFu);
           const int sl = (int)ws.wpre[p >> 5] + __popc(ws.bit[p >> 5] & ((1u << (p & 31)) - 1u));
+          SLC_CHECK(sl >= 0 && sl < s.k_eff && p < (uint32_t)s.len, "stage_R slot");
           ws.selpos[sl] = p;
           ws.selval[sl] = ws.candb[ci];
         }
@@ -360,6 +388,8 @@ struct Compressor {
 
   // ---- Q, F ----------------------------------------------------------------------------
   __device__ __forceinline__ void stage_Q(Sel& s) {
+    SLC_CHECK(s.c >= 0 && s.c < n_chunks, "stage_Q chunk");
+    SLC_CHECK(s.k_eff >= 1 && s.k_eff <= KMAX, "stage_Q k_eff");
     s.q = warp_quantize_pack<KC, IBC>(ws.selpos, ws.selval, ws.code, k, s.k_eff, g,
                                       records + s.c * g.rec_words, err);
   }
@@ -368,6 +398,8 @@ struct Compressor {
     for (int j = lane; j < s.k_eff; j += 32) {
       const int p = (int)ws.selpos[j];
       const float bb = ws.selval[j];
+      SLC_CHECK(p >= 0 && p < s.len, "stage_F position");
+      SLC_CHECK(pos_off<K::B>(s.d, p) < n_elems, "stage_F offset");
       const float mag = fabsf(bb) > s.q.tau ? s.q.fhi : s.q.flo;
       ef[pos_off<K::B>(s.d, p)] = __fsub_rn(bb, signbit(bb) ? -mag : mag);
     }
@@ -376,11 +408,14 @@ struct Compressor {
 
   // all stages, in order, for the chunk in s (whose dense e = b is stored)
   __device__ __forceinline__ void select(Sel& s, const uint32_t (&gk)[NP]) {
+#ifndef SLC_DBG_STAGES
+#define SLC_DBG_STAGES 5
+#endif
     stage_S(s, gk);
-    stage_B(s, gk);
-    stage_R(s);
-    stage_Q(s);
-    stage_F(s);
+    if (SLC_DBG_STAGES >= 2) stage_B(s, gk);
+    if (SLC_DBG_STAGES >= 3) stage_R(s);
+    if (SLC_DBG_STAGES >= 4) stage_Q(s);
+    if (SLC_DBG_STAGES >= 5) stage_F(s);
   }
 };
 
