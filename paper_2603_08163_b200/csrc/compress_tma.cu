@@ -4,7 +4,8 @@
 // stage ring.  Eq. 1.
 //
 // CTA = 1 producer warp + NC consumer warps, one CTA per SM.  CTA b owns the
-// chunks b, b+G, b+2G, ... (local index i).
+// chunks b, b+G, b+2G, ... (local index i); a consumer that becomes free
+// claims the next i (so stages are drained in order by whichever warp is idle).
 //  producer (one lane): for chunk i, wait until stage i % S is empty, arm its
 //    mbarrier with the chunk's byte count and issue three TMA copies — a 2-D
 //    tensor-map copy of the 64x64 block (theta, theta_local, e) for a
@@ -12,7 +13,7 @@
 //    partial chunk is only signalled (its consumer reads global memory).
 //    S stages of 48 KB (fp32) keep ~100+ KB per SM of HBM reads in flight
 //    with no registers or LSU work spent on them.
-//  consumer warp j: chunks i = j, j+NC, ...: wait for the stage, read theta,
+//  consumer warp: claim chunk i, wait for its stage, read theta,
 //    theta_local, e from shared memory (LDS.128, conflict-free), b =
 //    fma(beta, e, theta - theta_local) (R#12), store e <- b densely to HBM
 //    (L2 evict_last), keep the 256 group maxima, release the stage, then run
@@ -46,7 +47,7 @@ struct TmaCfg {
   static constexpr size_t off_scratch = S * stage_bytes;
   static constexpr size_t off_bar = off_scratch + kNC * sizeof(Scratch);
   static constexpr size_t off_rel = off_bar + 2 * S * sizeof(uint64_t);
-  static constexpr size_t bytes = off_rel + S * sizeof(int);
+  static constexpr size_t bytes = off_rel + (S + 1) * sizeof(int);  // rel[S], next claim
 };
 
 __device__ __forceinline__ void tma_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
   // on a stage several uses ahead — it first waits until the stage's previous
   // use has been released
   volatile int* rel = reinterpret_cast<volatile int*>(smem + T::off_rel);
+  int* next_claim = const_cast<int*>(rel) + S;  // consumers claim chunks in order as they become free
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t G = gridDim.x, n = a.n_chunks;
 
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
       ptx::mbar_init(&empty[s], 1);
       rel[s] = 0;
     }
+    *next_claim = 0;
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -123,7 +126,11 @@ __global__ void __launch_bounds__(32 * (kNC + 1), 1) compress_tma_kernel(const C
   Compressor<kC, BF16, 64, 12, kCapT, kKmaxT> cp(a, scratch, lane, 64);
   const uint64_t pol_last = l2_policy_evict_last();
 
-  for (int64_t i = cw;; i += kNC) {
+  (void)cw;
+  for (;;) {
+    int claim = 0;
+    if (lane == 0) claim = atomicAdd(next_claim, 1);
+    const int64_t i = __shfl_sync(kFull, claim, 0);
     const int64_t c = (int64_t)blockIdx.x + i * G;
     if (c >= n) break;
     const int s = (int)(i % S);
