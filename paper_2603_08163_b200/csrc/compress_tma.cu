@@ -31,14 +31,20 @@ namespace {
 using namespace wsel;
 
 constexpr int kC = 4096;
-constexpr int kNC = 12;          // consumer warps
+#ifndef SLC_TMA_NC
+#define SLC_TMA_NC 12
+#endif
+#ifndef SLC_TMA_S
+#define SLC_TMA_S 3
+#endif
+constexpr int kNC = SLC_TMA_NC;  // consumer warps
 constexpr int kCapT = 128;       // candidate capacity (k = 64)
 constexpr int kKmaxT = 64;
 
 template <bool BF16>
 struct TmaCfg {
   static constexpr int PB = BF16 ? 2 : 4;
-  static constexpr int S = BF16 ? 5 : 3;  // stages
+  static constexpr int S = BF16 ? SLC_TMA_S + 2 : SLC_TMA_S;  // stages
   static constexpr size_t arr_theta = 0;
   static constexpr size_t arr_tl = (size_t)kC * PB;
   static constexpr size_t arr_e = 2 * (size_t)kC * PB;
@@ -237,10 +243,14 @@ cudaError_t launch_tma(const CompressArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool compress_tma_supported(const Geom& g) {
-#ifdef SLC_NO_TMA  // tuning A/B builds only
+  // Off by default: measured slower than compress_warp.cu on B200 (the 48 KB
+  // stage ring caps the bytes in flight per SM at ~3 chunks).
+#ifdef SLC_USE_TMA
+  return g.C == kC && g.B == 64 && g.k == 64 && g.ib == 12;
+#else
+  (void)g;
   return false;
 #endif
-  return g.C == kC && g.B == 64 && g.k == 64 && g.ib == 12;
 }
 
 cudaError_t launch_compress_tma(const CompressArgs& a, int bf16, cudaStream_t s) {
