@@ -41,7 +41,7 @@ ALPHA = 1.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default=None)
     ap.add_argument("--R", type=int, default=None)
@@ -61,47 +61,53 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """`nvidia-smi -lms 100` in the background while the timed region runs:
+    SM clock median / max and any throttle reasons seen."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 6:
-                    self.samples.append(vals)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
+        self.out = ""
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample before the timed region starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        rows = [[v.strip() for v in ln.split(",")] for ln in self.out.strip().splitlines()]
+        rows = [r for r in rows if len(r) == 6]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def peak_hbm():
@@ -236,6 +242,10 @@ def run_slc(args):
     ms_total, ms_compress, ms_update = t.tolist()
     ms_step = ms_total / args.steps
 
+    extra = {}
+    if world > 1:
+        extra = time_collectives(plan, gather, shard, R, stream, dev)
+
     info = plan.info
     P_total = info.total_elems
     rb = info.record_bytes
@@ -280,11 +290,56 @@ def run_slc(args):
     }
     if e2e is not None:
         out["e2e"] = e2e
+    if extra:
+        out["collectives"] = extra
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(layout, R, dtype, args.cpu_seconds)
     if world > 1:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def time_collectives(plan, gather, shard, R, stream, dev, reps=5):
+    """a8 all-gather of the shard payloads alone, and the a9 simulated-peer
+    exchange (peer r's full message on rank r % n; each rank receives its slice
+    of every message) — both max over ranks, reported beside the step."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_08163_b200 import dist as sdist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    gather.start(shard.records)
+    gather.wait()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a.record(stream)
+    for _ in range(reps):
+        gather.start(shard.records)
+        gather.wait()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ag_ms = a.elapsed_time(b) / reps
+    ex = sdist.PeerExchange(gather, R)
+    owned = [gather.message for _ in range(rank, R, world)]  # every peer message: same bytes, same size
+    ex.run(owned)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a.record(stream)
+    for _ in range(reps):
+        ex.run(owned)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ex_ms = a.elapsed_time(b) / reps
+    t = torch.tensor([ag_ms, ex_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ag_ms, ex_ms = t.tolist()
+    msg = sum(gather.sizes)
+    return {"allgather_ms": ag_ms, "allgather_message_bytes": msg,
+            "allgather_busbw_gbs": msg * (world - 1) / world / (ag_ms * 1e-3) / 1e9,
+            "exchange_ms": ex_ms, "exchange_bytes_per_rank": R * plan.payload_bytes,
+            "note": "all-gather overlapped with the fused update inside the step; exchange (stand-in for the "
+                    "R2 download) reported separately, not in ms_per_step"}
 
 
 def run_e2e(args, plan, shard, recs, stream):
