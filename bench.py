@@ -362,7 +362,7 @@ def run_e2e(args, plan, shard, recs, stream):
             d.copy_(h, non_blocking=True)
         plan.compress(shard.theta, shard.theta_local, shard.ef, shard.records, beta=BETA, stream=stream)
         plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
-        own_host.copy_(shard.records, non_blocking=True)
+        own_host.copy_(recs[0], non_blocking=True)
 
     step()
     torch.cuda.synchronize()
