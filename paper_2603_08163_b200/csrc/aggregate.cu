@@ -47,8 +47,7 @@ template <int C>
 struct AggSmem {
   static constexpr size_t off_acc = 0;                                  // int2[C] or double[C]
   static constexpr size_t off_tab = sizeof(int2) * C;                   // int4[R]: lo/hi split of S_lo, S_hi
-  static constexpr size_t off_own = off_tab + sizeof(int4) * kMaxTable;  // u32[C / 32]: Delta written
-  static constexpr size_t off_rec = off_own + sizeof(uint32_t) * (C / 32);  // u32[R * RW + 1]
+  static constexpr size_t off_rec = off_tab + sizeof(int4) * kMaxTable;  // u32[R * RW + 1]
   static size_t bytes(int R, int RW, bool staged) {
     return off_rec + (staged ? sizeof(uint32_t) * ((size_t)R * RW + 1) : 0);
   }
@@ -65,7 +64,6 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
   double* accd = reinterpret_cast<double*>(smem + S::off_acc);   // weighted path
   int4* tab = reinterpret_cast<int4*>(smem + S::off_tab);
   uint32_t* srec = reinterpret_cast<uint32_t*>(smem + S::off_rec);
-  uint32_t* own = reinterpret_cast<uint32_t*>(smem + S::off_own);
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t chunk = blockIdx.x;
@@ -87,14 +85,10 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     const int k_eff = max(1, (a.g.k * len) / C);
     const int RW = a.g.rec_words, IW = a.g.idx_words, ib = a.g.ib;
     const bool staged = a.R * RW <= kRecSmemWords;
-    if (staged) {  // records -> smem with cp.async (no register round trip)
+    if (staged) {
       for (int r = warp; r < a.R; r += NT / 32) {
         const uint32_t* rec = a.rec[r] + chunk * RW;
-        for (int w = lane; w < RW; w += 32)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(
-                           srec + r * RW + w)),
-                       "l"(rec + w)
-                       : "memory");
+        for (int w = lane; w < RW; w += 32) srec[r * RW + w] = __ldcs(rec + w);
       }
       if (t == 0) srec[a.R * RW] = 0u;  // rec_index may read one word past the last record
     }
@@ -111,20 +105,10 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
         tab[r] = e4;
       }
       for (int i = t; i < C / 2; i += NT) reinterpret_cast<int4*>(acc)[i] = make_int4(0, 0, 0, 0);
-      for (int i = t; i < C / 32; i += NT) own[i] = 0u;
     } else {
       for (int i = t; i < C / 2; i += NT) reinterpret_cast<longlong2*>(accd)[i] = make_longlong2(0, 0);
     }
-    if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    if (mode == kFused) {  // theta's HBM latency overlaps the decode below
-#pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const int q = v * NT + t;
-        load_param4<BF16>(a.theta, group_offset(d, q, RPQ_SHIFT), valid_in_group(4 * q, len), &th[4 * v]);
-      }
-    }
-    const double invR = a.invR;
     if (!a.weighted) {
       const int total = a.R * k_eff;
       for (int s = t; s < total; s += NT) {
@@ -140,24 +124,6 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
         if ((int)p >= len) { bad = true; continue; }
         atomicAdd(&acc[p].x, lo);
         atomicAdd(&acc[p].y, hi);
-      }
-      __syncthreads();
-      // Delta once per touched position: the first entry of each position (elected
-      // with a bitmap) converts the exact sum and writes it back as fp32 bits into
-      // acc[p].x — no other thread reads acc[p] after the barrier above, and an
-      // untouched slot (0, 0) reads as +0.0f, the oracle's value for it
-      for (int s = t; s < total; s += NT) {
-        const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
-        const int j = s - r * k_eff;
-        const uint32_t* rec = staged ? srec + r * RW : a.rec[r] + chunk * RW;
-        const uint32_t p = rec_index(rec, j, ib);
-        if ((int)p >= len) continue;
-        const uint32_t bit = 1u << (p & 31);
-        if (atomicOr(&own[p >> 5], bit) & bit) continue;
-        const int2 q = acc[p];
-        const long long sum = (long long)q.y * (1ll << 20) + (long long)q.x;  // exact, |sum| < 2^53
-        const float dv = sum == 0 ? 0.0f : __double2float_rn(__dmul_rn(__dmul_rn((double)sum, 0x1p-24), invR));
-        acc[p].x = __float_as_int(dv);
       }
     } else if (t < 32) {
       for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
@@ -178,6 +144,7 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     }
     if (bad) atomicOr(a.err, kErrNonFinite);
     __syncthreads();
+    const double invR = a.invR;
 #pragma unroll
     for (int v = 0; v < 4; v++) {
       const int p0 = 4 * (v * NT + t);
@@ -187,10 +154,21 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
       } else {
         const int4 q0 = reinterpret_cast<const int4*>(acc)[(p0 >> 1)];
         const int4 q1 = reinterpret_cast<const int4*>(acc)[(p0 >> 1) + 1];
-        dl[4 * v + 0] = __int_as_float(q0.x);
-        dl[4 * v + 1] = __int_as_float(q0.z);
-        dl[4 * v + 2] = __int_as_float(q1.x);
-        dl[4 * v + 3] = __int_as_float(q1.z);
+        const int lo[4] = {q0.x, q0.z, q1.x, q1.z};
+        const int hi[4] = {q0.y, q0.w, q1.y, q1.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const long long s = (long long)hi[j] * (1ll << 20) + (long long)lo[j];
+          // exact: |s| < 2^53; untouched positions give +0 as in the oracle
+          dl[4 * v + j] = s == 0 ? 0.0f : __double2float_rn(__dmul_rn(__dmul_rn((double)s, 0x1p-24), invR));
+        }
+      }
+    }
+    if (mode == kFused) {
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int q = v * NT + t;
+        load_param4<BF16>(a.theta, group_offset(d, q, RPQ_SHIFT), valid_in_group(4 * q, len), &th[4 * v]);
       }
     }
   }
