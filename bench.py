@@ -110,6 +110,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def ncu_traffic(kernel: str, workload: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), if it was taken on this
+    workload; else None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        e = t.get(kernel)
+        if e and e.get("workload", "llama3.2-1b") == workload:
+            return e["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 def peak_hbm():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -282,7 +296,9 @@ def run_slc(args):
         "hbm_gbs": step_gbs_rank * world,
         "hbm_frac_of_peak": step_gbs_rank / peak,
         "roofline": {"bound": "hbm", "kernel": "slc_compress", "achieved": comp_gbs, "peak": peak,
-                     "unit": "GB/s", "frac": comp_gbs / peak, "traffic": None, "peak_source": peak_src},
+                     "unit": "GB/s", "frac": comp_gbs / peak,
+                     "traffic": ncu_traffic("compress", wl) if R == WORKLOADS[wl][1] else None,
+                     "algorithmic_bytes_per_launch": comp_bytes, "peak_source": peak_src},
         "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
                     "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
         "gpu_launches": 2 * args.steps,
