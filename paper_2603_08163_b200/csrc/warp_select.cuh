@@ -26,6 +26,23 @@
 #include "quant_pack.cuh"
 
 namespace slc {
+#ifdef SLC_PHASE_TIMING  // debug builds: per-phase SM cycles summed over warps (slc_debug_phase_cycles)
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_T0() long long _pt = clock64()
+#define PHASE_MARK(i)                                                         \
+  do {                                                                        \
+    long long _now = clock64();                                               \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_now - _pt)); \
+    _pt = _now;                                                               \
+  } while (0)
+#else
+#define PHASE_T0() \
+  do {             \
+  } while (0)
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
 namespace wsel {
 
 template <int C>
@@ -137,12 +154,6 @@ struct Compressor {
 
   // ---- B ---------------------------------------------------------------------------
   __device__ __forceinline__ void stage_B(Sel& s, const uint32_t (&gk)[NP]) {
-#ifdef SLC_DBG_B
-    if (lane == 0 && s.c < 2)
-      printf("stage_B chunk %lld ef=%p records=%p err=%p n_elems=%lld n_chunks=%lld k=%d lane=%d ws=%p\n",
-             (long long)s.c, (void*)ef, (void*)records, (void*)err, (long long)n_elems, (long long)n_chunks, k, lane,
-             (void*)&ws);
-#endif
     __syncwarp();  // e of chunk s.c (written by all lanes) is read back by other lanes
     uint32_t gmask = 0;
 #pragma unroll
@@ -162,49 +173,54 @@ struct Compressor {
         }
       }
       __syncwarp();
-      for (int r = 0; r < G; r += 32) {
-        const int gi = r + lane;
-        uint32_t cmask = 0;
-        int owner = 0, u = 0;
-        float vals[16];
-        if (gi < G) {
-          const uint32_t id = ws.hist[gi];
-          owner = (int)(id / NP);
-          u = (int)(id % NP);
-          SLC_CHECK(owner < 32 && u < NP, "stage_B group id");
+      // up to BR groups per lane are re-read at once: one L2 round trip, not BR
+      constexpr int BR = 3;
+      for (int r0 = 0; r0 < G; r0 += 32 * BR) {
+        float vals[BR][16];
+        int owner[BR], uu[BR];
 #pragma unroll
-          for (int v = 0; v < 4; v++) {
-            const int q = 128 * u + 32 * v + owner;
-            const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
-#ifdef SLC_DBG_B
-            {
-              const int64_t o = goff<K::RPQ_SHIFT>(s.d, q);
-              if (o < 0 || o + 4 > n_elems) {
-                printf("stage_B bad offset %lld chunk %lld owner %d u %d gi %d G %d base %lld ld %d len %d\n",
-                       (long long)o, (long long)s.c, owner, u, gi, G, (long long)s.d.base, s.d.ld, s.d.len);
-                for (int j = 0; j < 4; j++) vals[4 * v + j] = 0.0f;
-                continue;
-              }
+        for (int bq = 0; bq < BR; bq++) {
+          const int gi = r0 + 32 * bq + lane;
+          owner[bq] = 0;
+          uu[bq] = 0;
+          if (gi < G) {
+            const uint32_t id = ws.hist[gi];
+            owner[bq] = (int)(id / NP);
+            uu[bq] = (int)(id % NP);
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              const int q = 128 * uu[bq] + 32 * v + owner[bq];
+              load_f32x4(ef, goff<K::RPQ_SHIFT>(s.d, q), s.full ? 4 : valid_in_group(4 * q, s.len),
+                         &vals[bq][4 * v]);
             }
-#endif
-            load_f32x4(ef, goff<K::RPQ_SHIFT>(s.d, q), nv, &vals[4 * v]);
-#pragma unroll
-            for (int j = 0; j < 4; j++)
-              if (j < nv && key2_of(vals[4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
           }
         }
-        const int cc = __popc(cmask);
-        int o = M + warp_excl_scan(cc);
-        M += (int)__reduce_add_sync(kFull, (unsigned)cc);
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-          if ((cmask >> j) & 1u) {
-            const int p = 4 * (128 * u + 32 * (j >> 2) + owner) + (j & 3);
-            if (o < CAP) {
-              ws.cand[o] = ((uint64_t)key2_of(vals[j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
-              ws.candb[o] = vals[j];
+        for (int bq = 0; bq < BR; bq++) {
+          const int gi = r0 + 32 * bq + lane;
+          uint32_t cmask = 0;
+          if (gi < G) {
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              const int nv = s.full ? 4 : valid_in_group(4 * (128 * uu[bq] + 32 * v + owner[bq]), s.len);
+#pragma unroll
+              for (int j = 0; j < 4; j++)
+                if (j < nv && key2_of(vals[bq][4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
             }
-            o++;
+          }
+          const int cc = __popc(cmask);
+          int o = M + warp_excl_scan(cc);
+          M += (int)__reduce_add_sync(kFull, (unsigned)cc);
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            if ((cmask >> j) & 1u) {
+              const int p = 4 * (128 * uu[bq] + 32 * (j >> 2) + owner[bq]) + (j & 3);
+              if (o < CAP) {
+                ws.cand[o] = ((uint64_t)key2_of(vals[bq][j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
+                ws.candb[o] = vals[bq][j];
+              }
+              o++;
+            }
           }
         }
       }
@@ -408,14 +424,17 @@ struct Compressor {
 
   // all stages, in order, for the chunk in s (whose dense e = b is stored)
   __device__ __forceinline__ void select(Sel& s, const uint32_t (&gk)[NP]) {
-#ifndef SLC_DBG_STAGES
-#define SLC_DBG_STAGES 5
-#endif
+    PHASE_T0();
     stage_S(s, gk);
-    if (SLC_DBG_STAGES >= 2) stage_B(s, gk);
-    if (SLC_DBG_STAGES >= 3) stage_R(s);
-    if (SLC_DBG_STAGES >= 4) stage_Q(s);
-    if (SLC_DBG_STAGES >= 5) stage_F(s);
+    PHASE_MARK(1);
+    stage_B(s, gk);
+    PHASE_MARK(2);
+    stage_R(s);
+    PHASE_MARK(3);
+    stage_Q(s);
+    PHASE_MARK(4);
+    stage_F(s);
+    PHASE_MARK(5);
   }
 };
 

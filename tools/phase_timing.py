@@ -1,0 +1,33 @@
+"""Per-phase cycle breakdown of the compress warp kernel (SLC_PHASE_TIMING build)."""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import torch  # noqa: E402
+
+from helpers import make_device_inputs  # noqa: E402
+from paper_2603_08163_b200 import slc  # noqa: E402
+from slcgen import layouts  # noqa: E402
+
+lib = ctypes.CDLL(slc.LIB_PATH)
+layout = layouts.LAYOUTS[sys.argv[1] if len(sys.argv) > 1 else "llama3.2-1b"]
+plan = slc.Plan(layout)
+th, tl, ef = make_device_inputs(plan, layout, 1, 0, warm_ef=True)
+rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device="cuda")
+buf = (ctypes.c_ulonglong * 8)()
+plan.compress(th, tl, ef, rec)
+torch.cuda.synchronize()
+lib.slc_debug_phase_cycles(buf, 1)
+a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+a.record(); plan.compress(th, tl, ef, rec); b.record(); torch.cuda.synchronize()
+lib.slc_debug_phase_cycles(buf, 0)
+n = plan.n_chunks
+names = ["A stream", "S threshold", "B candidates", "R rank+slots", "Q quantise+pack", "F EF fix-ups"]
+tot = sum(buf[i] for i in range(6))
+print(f"kernel {a.elapsed_time(b):.3f} ms, {n} chunks; cycles per chunk per warp:")
+for i, nm in enumerate(names):
+    print(f"  {nm:18s} {buf[i] / n:10.0f}  {100 * buf[i] / tot:5.1f}%")
+print(f"  {'total':18s} {tot / n:10.0f}")
