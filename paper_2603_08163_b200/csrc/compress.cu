@@ -287,7 +287,12 @@ cudaError_t launch_compress(const CompressArgs& a, int bf16, cudaStream_t s) {
   if (a.n_chunks == 0) return cudaSuccess;
   switch (a.g.C) {
     case 1024:
-    case 4096: return launch_compress_warp(a, bf16, s);
+    case 4096:
+#ifdef SLC_NO_WS
+      return launch_compress_warp(a, bf16, s);
+#else
+      return launch_compress_ws(a, bf16, s);
+#endif
     case 16384: return bf16 ? launch_one<16384, true>(a, s) : launch_one<16384, false>(a, s);
   }
   return cudaErrorInvalidValue;

@@ -25,6 +25,7 @@ struct slc_plan {
   std::vector<slc_tensor> layout;
   std::vector<slc_segment> segs;
   int64_t total_elems = 0, total_chunks = 0, first_chunk = 0, n_chunks = 0, shard_elems = 0;
+  int64_t max_ld = 0;  // largest row length of a blocked segment
   ChunkDesc* d_chunks = nullptr;
   uint32_t* d_err = nullptr;
   // TMA: one (theta, theta_local, e) tensor-map triple per blocked segment,
@@ -303,6 +304,7 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
         const int64_t r0 = s.tensor_begin / cols, r1 = (s.tensor_begin + s.n_elems) / cols;
         s.rows = r1 - r0;
         s.cols = cols;
+        p->max_ld = std::max(p->max_ld, cols);
         s.first_chunk = chunk0 + (r0 / B) * nb;
         s.n_chunks = (s.rows / B) * nb;
         for (int64_t bi = 0; bi < s.rows / B; bi++)
@@ -408,6 +410,7 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   a.records = static_cast<uint32_t*>(records);
   a.err = p->d_err;
   a.beta = beta;
+  a.max_ld = p->max_ld;
   a.g = p->g;
   DeviceGuard guard(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

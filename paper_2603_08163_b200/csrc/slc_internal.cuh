@@ -64,6 +64,7 @@ struct CompressArgs {
   uint32_t* records;
   uint32_t* err;
   float beta;
+  int64_t max_ld;  // largest row length of a blocked chunk (32-bit in-chunk offsets if small)
   Geom g;
 };
 
@@ -91,6 +92,8 @@ cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t 
 cudaError_t launch_compress_simple(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one warp per chunk, no block-level synchronisation (C = 1024, 4096)
 cudaError_t launch_compress_warp(const CompressArgs& a, int param_bf16, cudaStream_t s);
+// persistent warp-specialised CTAs: stream warps + select warps (C = 1024, 4096)
+cudaError_t launch_compress_ws(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // TMA producer warp + warp-per-chunk consumers (C = 4096, k = 64, 12-bit indices)
 cudaError_t launch_compress_tma(const CompressArgs& a, int param_bf16, cudaStream_t s);
 bool compress_tma_supported(const Geom& g);

@@ -45,6 +45,10 @@ __device__ unsigned long long g_phase_cycles[8];
 #endif
 namespace wsel {
 
+#ifndef SLC_BR
+#define SLC_BR 3  // candidate groups re-read per lane per L2 round trip (stage B)
+#endif
+
 template <int C>
 struct WarpCfg {
   static constexpr int NP = C / 512;       // passes of 16 positions per lane
@@ -107,6 +111,115 @@ struct Sel {
   QuantOut q;
 };
 
+// exact k_eff-th largest key by 4 rounds of 8-bit radix select over all positions,
+// then key > K plus the first `need` positions with key == K (lower position wins)
+// (a free function: as a member its `this` would pin the Compressor in local memory)
+template <int C, int CAP, int KMAX>
+__device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+                                            const int len, const bool full, const int k_eff) {
+  using K = WarpCfg<C>;
+  constexpr int NP = K::NP;
+  WarpScratch<C, CAP, KMAX>& ws = *wsp;
+  uint32_t Kth = 0;
+  int need = k_eff;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) ws.hist[i] = 0u;
+    __syncwarp();
+    const uint32_t hi_mask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+#pragma unroll 1
+    for (int u = 0; u < NP; u++) {
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int q = 128 * u + 32 * v + lane;
+        const int nv = full ? 4 : valid_in_group(4 * q, len);
+        float ev[4];
+        load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t key = key2_of(ev[j]);
+          if (j < nv && (key & hi_mask) == (Kth & hi_mask)) atomicAdd(&ws.hist[(key >> shift) & 255u], 1u);
+        }
+      }
+    }
+    __syncwarp();
+    // digit D: #(digit > D) < need <= #(digit >= D); lane l holds bins 8l..8l+7
+    uint32_t h[8];
+    uint32_t s8 = 0;
+#pragma unroll
+    for (int x = 0; x < 8; x++) { h[x] = ws.hist[8 * lane + x]; s8 += h[x]; }
+    uint32_t inc = s8;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(kFull, inc, o);
+      if (lane + o < 32) inc += y;
+    }
+    uint32_t acc = inc - s8;  // bins in lanes above
+    int found = -1;
+    uint32_t found_gt = 0;
+#pragma unroll
+    for (int x = 7; x >= 0; x--) {
+      if (found < 0 && acc < (uint32_t)need && acc + h[x] >= (uint32_t)need) { found = 8 * lane + x; found_gt = acc; }
+      acc += h[x];
+    }
+    const int src = __ffs(__ballot_sync(kFull, found >= 0)) - 1;
+    Kth |= (uint32_t)__shfl_sync(kFull, found, src) << shift;
+    need -= (int)__shfl_sync(kFull, found_gt, src);
+    __syncwarp();
+  }
+  int taken = 0;
+#pragma unroll 1
+  for (int u = 0; u < NP; u++) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
+      const int q = 128 * u + 32 * v + lane;
+      const int nv = full ? 4 : valid_in_group(4 * q, len);
+      float ev[4];
+      load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
+      uint32_t tmask = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint32_t key = key2_of(ev[j]);
+        if (j < nv && key > Kth) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
+        if (j < nv && key == Kth) tmask |= 1u << j;
+      }
+      const int tc = __popc(tmask);
+      int o = taken + warp_excl_scan(tc);
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if ((tmask >> j) & 1u) {
+          if (o < need) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
+          o++;
+        }
+      }
+      taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
+    }
+  }
+  __syncwarp();
+  // slots in ascending position; values re-read from e (= b, written by the stream)
+  constexpr int WPL = K::BW / 32;
+  uint32_t w[WPL];
+  int cw = 0;
+#pragma unroll
+  for (int x = 0; x < WPL; x++) { w[x] = ws.bit[WPL * lane + x]; cw += __popc(w[x]); }
+  int pre = warp_excl_scan(cw);
+#pragma unroll
+  for (int x = 0; x < WPL; x++) {
+    uint32_t y = w[x];
+    while (y) {
+      const int bp = __ffs(y) - 1;
+      y &= y - 1;
+      const int p = 32 * (WPL * lane + x) + bp;
+      if (pre < KMAX) {
+        ws.selpos[pre] = (uint32_t)p;
+        ws.selval[pre] = ef[pos_off<K::B>(d, p)];
+      }
+      pre++;
+    }
+  }
+}
+
 template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
 struct Compressor {
   using K = WarpCfg<C>;
@@ -141,7 +254,7 @@ struct Compressor {
     s.bad = __reduce_max_sync(kFull, gmaxk) >= 0xFF000001u;  // |b| = inf or NaN somewhere
     if (s.bad && lane == 0) atomicOr(err, kErrNonFinite);
     uint32_t T = 0;
-#pragma unroll
+#pragma unroll 1
     for (int bit = 31; bit >= 14; --bit) {
       const uint32_t Tp = T | (1u << bit);
       int cnt = 0;
@@ -174,7 +287,7 @@ struct Compressor {
       }
       __syncwarp();
       // up to BR groups per lane are re-read at once: one L2 round trip, not BR
-      constexpr int BR = 3;
+      constexpr int BR = SLC_BR;
       for (int r0 = 0; r0 < G; r0 += 32 * BR) {
         float vals[BR][16];
         int owner[BR], uu[BR];
@@ -294,112 +407,9 @@ struct Compressor {
         }
       }
     } else {
-      fallback(s.d, s.len, s.full, s.k_eff);
+      radix_fallback<C, CAP, KMAX>(ef, &ws, lane, s.d, s.len, s.full, s.k_eff);
     }
     __syncwarp();
-  }
-
-  // exact k_eff-th largest key by 4 rounds of 8-bit radix select over all positions,
-  // then key > K plus the first `need` positions with key == K (lower position wins)
-  __device__ __noinline__ void fallback(const ChunkDesc d, const int len, const bool full, const int k_eff) {
-    uint32_t Kth = 0;
-    int need = k_eff;
-#pragma unroll 1
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = lane; i < 256; i += 32) ws.hist[i] = 0u;
-      __syncwarp();
-      const uint32_t hi_mask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-#pragma unroll 1
-      for (int u = 0; u < NP; u++) {
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-          const int q = 128 * u + 32 * v + lane;
-          const int nv = full ? 4 : valid_in_group(4 * q, len);
-          float ev[4];
-          load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const uint32_t key = key2_of(ev[j]);
-            if (j < nv && (key & hi_mask) == (Kth & hi_mask)) atomicAdd(&ws.hist[(key >> shift) & 255u], 1u);
-          }
-        }
-      }
-      __syncwarp();
-      // digit D: #(digit > D) < need <= #(digit >= D); lane l holds bins 8l..8l+7
-      uint32_t h[8];
-      uint32_t s8 = 0;
-#pragma unroll
-      for (int x = 0; x < 8; x++) { h[x] = ws.hist[8 * lane + x]; s8 += h[x]; }
-      uint32_t inc = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_down_sync(kFull, inc, o);
-        if (lane + o < 32) inc += y;
-      }
-      uint32_t acc = inc - s8;  // bins in lanes above
-      int found = -1;
-      uint32_t found_gt = 0;
-#pragma unroll
-      for (int x = 7; x >= 0; x--) {
-        if (found < 0 && acc < (uint32_t)need && acc + h[x] >= (uint32_t)need) { found = 8 * lane + x; found_gt = acc; }
-        acc += h[x];
-      }
-      const int src = __ffs(__ballot_sync(kFull, found >= 0)) - 1;
-      Kth |= (uint32_t)__shfl_sync(kFull, found, src) << shift;
-      need -= (int)__shfl_sync(kFull, found_gt, src);
-      __syncwarp();
-    }
-    int taken = 0;
-#pragma unroll 1
-    for (int u = 0; u < NP; u++) {
-#pragma unroll
-      for (int v = 0; v < 4; v++) {
-        // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
-        const int q = 128 * u + 32 * v + lane;
-        const int nv = full ? 4 : valid_in_group(4 * q, len);
-        float ev[4];
-        load_f32x4(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
-        uint32_t tmask = 0;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const uint32_t key = key2_of(ev[j]);
-          if (j < nv && key > Kth) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
-          if (j < nv && key == Kth) tmask |= 1u << j;
-        }
-        const int tc = __popc(tmask);
-        int o = taken + warp_excl_scan(tc);
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          if ((tmask >> j) & 1u) {
-            if (o < need) atomicOr(&ws.bit[(4 * q + j) >> 5], 1u << ((4 * q + j) & 31));
-            o++;
-          }
-        }
-        taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
-      }
-    }
-    __syncwarp();
-    // slots in ascending position; values re-read from e (= b, written by the stream)
-    constexpr int WPL = K::BW / 32;
-    uint32_t w[WPL];
-    int cw = 0;
-#pragma unroll
-    for (int x = 0; x < WPL; x++) { w[x] = ws.bit[WPL * lane + x]; cw += __popc(w[x]); }
-    int pre = warp_excl_scan(cw);
-#pragma unroll
-    for (int x = 0; x < WPL; x++) {
-      uint32_t y = w[x];
-      while (y) {
-        const int bp = __ffs(y) - 1;
-        y &= y - 1;
-        const int p = 32 * (WPL * lane + x) + bp;
-        if (pre < KMAX) {
-          ws.selpos[pre] = (uint32_t)p;
-          ws.selval[pre] = ef[pos_off<K::B>(d, p)];
-        }
-        pre++;
-      }
-    }
   }
 
   // ---- Q, F ----------------------------------------------------------------------------

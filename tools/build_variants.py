@@ -10,12 +10,24 @@ import __graft_entry__ as ge  # noqa: E402
 
 
 def build(name, defines):
+    """defines: -D macros; an entry "@<git rev>" builds that revision's csrc/ instead."""
     out_dir = os.path.join(ROOT, "build", "variants")
     os.makedirs(out_dir, exist_ok=True)
     out = os.path.join(out_dir, f"libslc_{name}.so")
     csrc = os.path.join(ge.PKG, "csrc")
+    revs = [d[1:] for d in defines if d.startswith("@")]
+    defines = [d for d in defines if not d.startswith("@")]
+    if revs:
+        tmp = os.path.join(out_dir, f"src_{name}")
+        os.makedirs(tmp, exist_ok=True)
+        rel = os.path.relpath(csrc, ROOT)
+        subprocess.check_call(f"git -C {ROOT} archive {revs[0]} {rel} include | tar -x -C {tmp}", shell=True)
+        csrc = os.path.join(tmp, rel)
+    srcs = ge.SLC_SOURCES
+    if revs:
+        srcs = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cpp")))
     cmd = [ge.NVCC, *ge.ARCH, *ge.NVFLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           "-o", out, *[os.path.join(csrc, s) for s in ge.SLC_SOURCES]]
+           "-o", out, *[os.path.join(csrc, s) for s in srcs]]
     subprocess.check_call(cmd)
     return out
 

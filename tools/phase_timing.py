@@ -20,13 +20,15 @@ rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device="cuda")
 buf = (ctypes.c_ulonglong * 8)()
 plan.compress(th, tl, ef, rec)
 torch.cuda.synchronize()
-lib.slc_debug_phase_cycles(buf, 1)
+fn = getattr(lib, "slc_debug_phase_cycles_ws" if os.environ.get("WS") else "slc_debug_phase_cycles")
+fn(buf, 1)
 a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
 a.record(); plan.compress(th, tl, ef, rec); b.record(); torch.cuda.synchronize()
-lib.slc_debug_phase_cycles(buf, 0)
+fn(buf, 0)
 n = plan.n_chunks
-names = ["A stream", "S threshold", "B candidates", "R rank+slots", "Q quantise+pack", "F EF fix-ups"]
-tot = sum(buf[i] for i in range(6))
+names = ["A stream", "S threshold", "B candidates", "R rank+slots", "Q quantise+pack", "F EF fix-ups",
+         "stream: wait empty", "select: wait full"]
+tot = sum(buf[i] for i in range(8))
 print(f"kernel {a.elapsed_time(b):.3f} ms, {n} chunks; cycles per chunk per warp:")
 for i, nm in enumerate(names):
     print(f"  {nm:18s} {buf[i] / n:10.0f}  {100 * buf[i] / tot:5.1f}%")
