@@ -1,0 +1,393 @@
+// aggregate_pipe.cu — persistent, software-pipelined decode / aggregate (/ outer
+// update) kernel: Eq. 2 of PAPER.md, the same arithmetic as
+// aggregate.cu (R#17, R#18) with the HBM latency hidden.
+//
+// The one-CTA-per-chunk kernel (aggregate.cu) runs its phases back to back —
+// records in, scatter, theta in, theta out — so theta's HBM round trip is
+// exposed once per chunk, and it converts all C accumulator entries although
+// at most R*k of them were touched (ncu: 4.6 TB/s, 67 % issue-active).  Here a
+// CTA of C/16 threads walks chunks c = blockIdx.x + i*gridDim.x and, while it
+// works on chunk i, already has chunk i+1's theta loads (registers) and records
+// (cp.async into the other shared-memory buffer) in flight; descriptors are
+// loaded three chunks ahead, so no load waits on another.  Per thread: 16
+// positions in 4 groups of 4 (chunk_io.cuh mapping), theta double-buffered in
+// registers (2 x 16 fp32).
+//
+// Per chunk, with E = R * k_eff entries:
+//   pass 1  every entry -> exact fixed-point accumulator acc[p] (shared
+//           atomics), its position remembered in spos[]
+//   pass 2  every entry: Delta[p] = (float)(acc[p] * 2^-24 * (1/R)) -> dlt[p]
+//           (duplicates write the same value); untouched dlt stay +0
+//   pass 3  dense: theta <- fma(-alpha, dlt, theta), dlt re-zeroed; acc
+//           re-zeroed at the E touched positions only
+// Accumulation is exact (R#17) exactly as in aggregate.cu: each fp16 scale is
+// an integer multiple of 2^-24, split hi*2^20 + lo into two 32-bit shared
+// counters with native atomics; hi*2^20 + lo < 2^53 is formed exactly in fp64
+// and multiplied once by 2^-24 * invR (exact), which is the oracle's
+// (float)(acc * invR).  fma(-alpha, +0, theta) == theta for every theta, so the
+// dense pass needs no special case.  Weighted mode (median-norm weights,
+// P:101): fp64 in canonical peer order, one warp walking the peers.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "chunk_io.cuh"
+
+namespace slc {
+namespace {
+
+__device__ __forceinline__ long long f16_fixed24(uint32_t h) {
+  const uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
+  return e == 0 ? (long long)m : (long long)(1024u + m) << (e - 1);
+}
+
+__device__ __forceinline__ uint32_t rec_index(const uint32_t* rec, int j, int ib) {
+  const int bit = ib * j;
+  const int w = bit >> 5, sh = bit & 31;
+  return __funnelshift_r(rec[w], rec[w + 1], sh) & ((1u << ib) - 1u);
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// words of one record buffer (all R records of a chunk + 1 pad word), 16-B multiple
+__host__ __device__ inline int rec_buf_words(int R, int RW) { return ((R * RW + 1) + 3) & ~3; }
+
+template <int C>
+struct PipeSmem {
+  static constexpr size_t off_acc = 0;                 // int2[C] / double[C]
+  static constexpr size_t off_dlt = sizeof(int2) * C;  // float[C]: Delta
+  static constexpr size_t off_pos = off_dlt + sizeof(float) * C;  // u16[R * k]: entry positions
+  __host__ __device__ static size_t off_rec(int R, int k) {
+    return off_pos + ((sizeof(uint16_t) * R * k + 15) & ~size_t(15));
+  }
+  __host__ __device__ static size_t off_desc(int R, int k, int RW) {
+    return off_rec(R, k) + 2 * sizeof(uint32_t) * rec_buf_words(R, RW);
+  }
+  __host__ __device__ static size_t bytes(int R, int k, int RW) { return off_desc(R, k, RW) + 4 * 16; }
+};
+
+#ifndef SLC_AGG_MINB
+#define SLC_AGG_MINB 3  // CTAs per SM the register budget is sized for (C = 4096)
+#endif
+
+template <int C>
+struct PipeCfg {
+  static constexpr int NT = C / 16;
+  static constexpr int MIN_BLOCKS = (C == 4096) ? SLC_AGG_MINB : 4 * SLC_AGG_MINB;
+  static constexpr int RPQ = ChunkCfg<C>::RPQ;  // 4-element groups per block row
+  static constexpr int RPQ_SHIFT = (RPQ == 8) ? 3 : (RPQ == 16 ? 4 : 5);
+};
+
+// the 16 bytes of a chunk descriptor the update needs
+struct Desc {
+  int64_t base;
+  int32_t ld, len;
+};
+
+__device__ __forceinline__ Desc unpack_desc(const int4 v) {
+  Desc d;
+  d.base = (int64_t)(((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x);
+  d.ld = v.z;
+  d.len = v.w;
+  return d;
+}
+
+// element offset of thread t's group v is o + v * step (full chunks)
+template <int C>
+__device__ __forceinline__ void full_addr(const Desc& d, int t, int64_t& o, int64_t& step) {
+  using K = PipeCfg<C>;
+  if (d.ld) {
+    o = d.base + (int64_t)(t >> K::RPQ_SHIFT) * d.ld + 4 * (t & (K::RPQ - 1));
+    step = (int64_t)(K::NT / K::RPQ) * d.ld;
+  } else {
+    o = d.base + 4 * t;
+    step = 4 * K::NT;
+  }
+}
+
+__device__ __forceinline__ int64_t generic_offset(const Desc& d, int q, int rpq_shift) {
+  return d.ld ? d.base + (int64_t)(q >> rpq_shift) * d.ld + 4 * (q & ((1 << rpq_shift) - 1))
+              : d.base + 4 * (int64_t)q;
+}
+
+template <int C, bool BF16>
+__device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int t, float th[16]) {
+  using K = PipeCfg<C>;
+  if (d.len == C) {
+    int64_t o, step;
+    full_addr<C>(d, t, o, step);
+#pragma unroll
+    for (int v = 0; v < 4; v++) load_param4<BF16>(theta, o + v * step, 4, &th[4 * v]);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const int q = v * K::NT + t;
+      load_param4<BF16>(theta, generic_offset(d, q, K::RPQ_SHIFT), valid_in_group(4 * q, d.len), &th[4 * v]);
+    }
+  }
+}
+
+// all R records of chunk c -> srec (cp.async, 4 B each; records are 4-B aligned)
+template <int NT>
+__device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint32_t* srec, int t) {
+  const int RW = a.g.rec_words;
+  const int lane = t & 31, warp = t >> 5;
+  for (int r = warp; r < a.R; r += NT / 32) {
+    const uint32_t* rec = a.rec[r] + c * RW;
+    for (int w = lane; w < RW; w += 32) cp_async4(srec + r * RW + w, rec + w);
+  }
+}
+
+template <int C, bool BF16, int MODE>
+struct Pipe {
+  using K = PipeCfg<C>;
+  static constexpr int NT = K::NT;
+
+  const AggArgs& a;
+  int2* acc;
+  double* accd;
+  float* dlt;
+  uint16_t* spos;
+  uint32_t* srec0;
+  int bufw;
+  int t;
+  int64_t n, G;
+  int64_t c;
+  int4* ring;  // descriptors (first 16 B) of chunks c, c+G, c+2G, c+3G: slot = step & 3
+  int it;      // step counter
+  int buf;
+  bool bad;
+
+  // one chunk: `cur` holds chunk c's theta, `nxt` receives chunk c+G's
+  __device__ __forceinline__ bool step(float (&cur)[16], float (&nxt)[16]) {
+    const int64_t cn = c + G;
+    const bool has_next = cn < n;
+    // descriptors travel through shared memory by cp.async, three chunks ahead:
+    // a register load would be consumed (uniform-register move) at once
+    if (has_next) {
+      if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(ring[(it + 1) & 3]), t, nxt);
+      issue_records<NT>(a, cn, srec0 + (buf ^ 1) * bufw, t);
+    }
+    if (t == 0 && cn + 2 * G < n) cp_async16(&ring[(it + 3) & 3], a.chunks + cn + 2 * G);
+    cp_async_commit();
+    const Desc d0 = unpack_desc(ring[it & 3]);
+
+    const uint32_t* srec = srec0 + buf * bufw;
+    const int len = d0.len;
+    const int k_eff = max(1, (a.g.k * len) / C);
+    const int RW = a.g.rec_words, IW = a.g.idx_words, ib = a.g.ib;
+    const int total = a.R * k_eff;
+    cp_async_wait1();
+    __syncthreads();  // chunk c's records visible; previous chunk's passes done
+
+    if (!a.weighted) {
+      // pass 1: every entry into the exact accumulator; remember its position
+      for (int s = t; s < total; s += NT) {
+        const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
+        const int j = s - r * k_eff;
+        const uint32_t* rec = srec + r * RW;
+        uint32_t p = rec_index(rec, j, ib);
+        const uint32_t code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
+        const uint32_t sw = rec[RW - 1];
+        const uint32_t h = (code & 2u) ? (sw >> 16) : (sw & 0xFFFFu);
+        const long long f = f16_fixed24(h);
+        int lo = (int)(f & 0xFFFFF), hi = (int)(f >> 20);
+        if (code & 1u) { lo = -lo; hi = -hi; }
+        if ((int)p >= len || ((h >> 10) & 0x1Fu) == 0x1Fu) { bad = true; p = 0; lo = 0; hi = 0; }
+        spos[s] = (uint16_t)p;
+        atomicAdd(&acc[p].x, lo);
+        atomicAdd(&acc[p].y, hi);
+      }
+    } else {
+      for (int s = t; s < total; s += NT) {
+        const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
+        const uint32_t p = rec_index(srec + r * RW, s - r * k_eff, ib);
+        spos[s] = (int)p < len ? (uint16_t)p : (uint16_t)0;
+      }
+      if (t < 32) {
+        for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
+          const uint32_t* rec = srec + i * RW;
+          const double w = (double)a.w[i];
+          const uint32_t sw = rec[RW - 1];
+          for (int j = t; j < k_eff; j += 32) {
+            const uint32_t p = rec_index(rec, j, ib);
+            const uint32_t code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
+            const uint32_t h = (code & 2u) ? (sw >> 16) : (sw & 0xFFFFu);
+            if ((int)p >= len || ((h >> 10) & 0x1Fu) == 0x1Fu) { bad = true; continue; }
+            float dq = __half2float(__ushort_as_half((unsigned short)h));
+            if (code & 1u) dq = -dq;
+            accd[p] = __dadd_rn(accd[p], __dmul_rn(w, (double)dq));
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();  // scatter complete
+
+    // pass 2: Delta only at touched positions (duplicates write the same value)
+    const double invR = a.invR;
+    const double c24 = invR * 0x1p-24;  // exact (power-of-two scaling)
+    for (int s = t; s < total; s += NT) {
+      const int p = spos[s];
+      const int2 v = acc[p];
+      float d;
+      if (a.weighted) {
+        d = __double2float_rn(__dmul_rn(__hiloint2double(v.y, v.x), invR));
+      } else {
+        // exact: hi*2^20 + lo (|.| < 2^53) is representable; one rounding in the product
+        const double sd = __fma_rn((double)v.y, 0x1p20, (double)v.x);
+        d = sd == 0.0 ? 0.0f : __double2float_rn(__dmul_rn(sd, c24));
+      }
+      dlt[p] = d;
+    }
+    __syncthreads();  // Delta complete
+
+    // pass 3: dense, untouched positions hold +0
+    const float alpha = a.alpha;
+    if (len == C) {
+      int64_t o, stp;
+      full_addr<C>(d0, t, o, stp);
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        float4* d4 = reinterpret_cast<float4*>(dlt) + v * NT + t;
+        const float4 dv = *d4;
+        *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const float dl[4] = {dv.x, dv.y, dv.z, dv.w};
+        if (MODE == kAggOnly) {
+          store_f32x4(a.agg, o + v * stp, 4, dl);
+        } else {
+          float th[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) th[j] = __fmaf_rn(-alpha, dl[j], cur[4 * v + j]);
+          store_param4<BF16>(a.theta, o + v * stp, 4, th);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int q = v * NT + t;
+        float4* d4 = reinterpret_cast<float4*>(dlt) + q;
+        const float4 dv = *d4;
+        *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const float dl[4] = {dv.x, dv.y, dv.z, dv.w};
+        const int nv = valid_in_group(4 * q, len);
+        if (nv == 0) continue;
+        const int64_t off = generic_offset(d0, q, K::RPQ_SHIFT);
+        if (MODE == kAggOnly) {
+          store_f32x4(a.agg, off, nv, dl);
+        } else {
+          float th[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) th[j] = __fmaf_rn(-alpha, dl[j], cur[4 * v + j]);
+          store_param4<BF16>(a.theta, off, nv, th);
+        }
+      }
+    }
+    // the accumulator is re-zeroed where it was touched (the next scatter follows a barrier)
+    for (int s = t; s < total; s += NT) acc[spos[s]] = make_int2(0, 0);
+
+    c = cn;
+    it++;
+    buf ^= 1;
+    return has_next;
+  }
+};
+
+template <int C, bool BF16, int MODE>
+__global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pipe_kernel(const AggArgs a) {
+  using S = PipeSmem<C>;
+  constexpr int NT = PipeCfg<C>::NT;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int t = threadIdx.x;
+  Pipe<C, BF16, MODE> P{a};
+  P.acc = reinterpret_cast<int2*>(smem + S::off_acc);
+  P.accd = reinterpret_cast<double*>(smem + S::off_acc);
+  P.dlt = reinterpret_cast<float*>(smem + S::off_dlt);
+  P.spos = reinterpret_cast<uint16_t*>(smem + S::off_pos);
+  P.srec0 = reinterpret_cast<uint32_t*>(smem + S::off_rec(a.R, a.g.k));
+  P.bufw = rec_buf_words(a.R, a.g.rec_words);
+  P.t = t;
+  P.n = a.n_chunks;
+  P.G = gridDim.x;
+  P.c = blockIdx.x;
+  P.buf = 0;
+  P.it = 0;
+  P.bad = false;
+  P.ring = reinterpret_cast<int4*>(smem + S::off_desc(a.R, a.g.k, a.g.rec_words));
+  if (P.c >= P.n) return;
+
+  for (int i = t; i < C / 2; i += NT) reinterpret_cast<int4*>(P.acc)[i] = make_int4(0, 0, 0, 0);
+  for (int i = t; i < C / 4; i += NT) reinterpret_cast<float4*>(P.dlt)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (t < 2) P.srec0[t * P.bufw + a.R * a.g.rec_words] = 0u;  // rec_index may read one word past the last record
+
+  if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
+  __syncthreads();
+  float thA[16], thB[16];
+  if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(P.ring[0]), t, thA);
+  issue_records<NT>(a, P.c, P.srec0, t);
+  cp_async_commit();
+
+  for (;;) {
+    if (!P.step(thA, thB)) break;
+    if (!P.step(thB, thA)) break;
+  }
+  if (P.bad) atomicOr(a.err, kErrNonFinite);
+}
+
+template <int C, bool BF16, int MODE>
+cudaError_t launch_pipe(const AggArgs& a, cudaStream_t s) {
+  if (a.R > kMaxPeers) return cudaErrorInvalidValue;
+  auto kern = agg_pipe_kernel<C, BF16, MODE>;
+  const size_t smem = PipeSmem<C>::bytes(a.R, a.g.k, a.g.rec_words);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PipeCfg<C>::NT, smem)) != cudaSuccess)
+    return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t grid = std::min<int64_t>(a.n_chunks, (int64_t)sms * per_sm);
+  // test knob: cap the grid so that every CTA walks many chunks (pipeline hand-offs)
+  if (const char* cap = std::getenv("SLC_AGG_GRID")) grid = std::max<int64_t>(1, std::min<int64_t>(grid, atoll(cap)));
+  kern<<<(unsigned)grid, PipeCfg<C>::NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool aggregate_pipe_supported(const AggArgs& a) {
+  if (a.g.C != 1024 && a.g.C != 4096) return false;
+  const size_t smem = a.g.C == 1024 ? PipeSmem<1024>::bytes(a.R, a.g.k, a.g.rec_words)
+                                    : PipeSmem<4096>::bytes(a.R, a.g.k, a.g.rec_words);
+  return smem <= 200 * 1024;  // leaves room for 1 CTA per SM with any driver reservation
+}
+
+cudaError_t launch_aggregate_pipe(const AggArgs& a, int bf16, cudaStream_t s) {
+  if (a.n_chunks == 0) return cudaSuccess;
+  if (a.mode != kFused && a.mode != kAggOnly) return cudaErrorInvalidValue;
+  const bool fused = a.mode == kFused;
+  switch (a.g.C) {
+    case 1024:
+      if (fused) return bf16 ? launch_pipe<1024, true, kFused>(a, s) : launch_pipe<1024, false, kFused>(a, s);
+      return launch_pipe<1024, false, kAggOnly>(a, s);
+    case 4096:
+      if (fused) return bf16 ? launch_pipe<4096, true, kFused>(a, s) : launch_pipe<4096, false, kFused>(a, s);
+      return launch_pipe<4096, false, kAggOnly>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace slc

@@ -98,6 +98,9 @@ cudaError_t launch_compress_ws(const CompressArgs& a, int param_bf16, cudaStream
 cudaError_t launch_compress_tma(const CompressArgs& a, int param_bf16, cudaStream_t s);
 bool compress_tma_supported(const Geom& g);
 cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
+// persistent software-pipelined decode / fused update (C = 1024, 4096)
+cudaError_t launch_aggregate_pipe(const AggArgs& a, int param_bf16, cudaStream_t s);
+bool aggregate_pipe_supported(const AggArgs& a);
 bool compress_supported(int C);
 
 }  // namespace slc

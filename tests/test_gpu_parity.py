@@ -22,6 +22,20 @@ from paper_2603_08163_b200 import slc  # noqa: E402
 DEV = torch.device("cuda:0")
 
 
+# the two decode/update kernels: the persistent pipelined one (default; with a
+# capped grid every CTA walks many chunks) and the one-CTA-per-chunk one
+AGG_KERNELS = {"pipe": {}, "pipe-grid3": {"SLC_AGG_GRID": "3"}, "simple": {"SLC_AGG_KERNEL": "simple"}}
+
+
+@pytest.fixture(params=sorted(AGG_KERNELS))
+def agg_kernel(request, monkeypatch):
+    monkeypatch.delenv("SLC_AGG_KERNEL", raising=False)
+    monkeypatch.delenv("SLC_AGG_GRID", raising=False)
+    for k, v in AGG_KERNELS[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
 def _compress_gpu(plan, layout, seed, peer, dtype, special_period, warm, theta=None):
     theta, tl, ef = make_device_inputs(plan, layout, seed, peer, dtype, special_period, warm, theta=theta)
     rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
@@ -49,7 +63,7 @@ def test_compress_parity(name, dtype, special):
 
 @pytest.mark.parametrize("R", [1, 3, 8, 20])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_aggregate_update_parity(R, dtype):
+def test_aggregate_update_parity(R, dtype, agg_kernel):
     layout = layouts.LAYOUTS["ragged"]
     plan = slc.Plan(layout, dtype=dtype)
     recs, ref_recs = [], []
@@ -84,7 +98,7 @@ def test_aggregate_update_parity(R, dtype):
         assert np.array_equal(bits(un.numpy()), tb)
 
 
-def test_permutation_invariance_and_weights():
+def test_permutation_invariance_and_weights(agg_kernel):
     layout = layouts.LAYOUTS["ragged"]
     plan = slc.Plan(layout)
     R = 12
@@ -142,7 +156,7 @@ def test_sharding_invariance(nranks):
 
 
 @pytest.mark.parametrize("block,k", [(32, 16), (64, 16), (64, 32), (64, 128), (64, 256), (128, 256)])
-def test_geometry_sweep_parity(block, k):
+def test_geometry_sweep_parity(block, k, agg_kernel):
     g = slc.geometry(block=block, k=k)
     og = oracle.geom(block=block, k=k)
     B = block
