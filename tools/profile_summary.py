@@ -67,7 +67,7 @@ def full(rep, out, units=None):
         scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
         rd *= scale.get(unitrow[h.index("dram__bytes_read.sum")], 1)
         wr *= scale.get(unitrow[h.index("dram__bytes_write.sum")], 1)
-        short = "compress" if "compress" in name else ("aggregate" if "aggregate" in name else name)
+        short = "compress" if "compress" in name else ("aggregate" if ("aggregate" in name or "agg_pipe" in name) else name)
         traffic[short] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "kernel": name,
                           "source": os.path.basename(rep)}
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
