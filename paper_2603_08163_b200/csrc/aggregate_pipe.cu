@@ -16,17 +16,20 @@
 // Per chunk, with E = R * k_eff entries:
 //   pass 1  every entry -> exact fixed-point accumulator acc[p] (shared
 //           atomics), its position remembered in spos[]
-//   pass 2  every entry: Delta[p] = (float)(acc[p] * 2^-24 * (1/R)) -> dlt[p]
-//           (duplicates write the same value); untouched dlt stay +0
+//   pass 2  every entry: Delta[p] = (float)(acc[p] * 2^-24 * (1/R)) -> dlt[p];
+//           untouched dlt stay +0
 //   pass 3  dense: theta <- fma(-alpha, dlt, theta), dlt re-zeroed; acc
 //           re-zeroed at the E touched positions only
-// Accumulation is exact (R#17) exactly as in aggregate.cu: each fp16 scale is
-// an integer multiple of 2^-24, split hi*2^20 + lo into two 32-bit shared
-// counters with native atomics; hi*2^20 + lo < 2^53 is formed exactly in fp64
-// and multiplied once by 2^-24 * invR (exact), which is the oracle's
-// (float)(acc * invR).  fma(-alpha, +0, theta) == theta for every theta, so the
-// dense pass needs no special case.  Weighted mode (median-norm weights,
-// P:101): fp64 in canonical peer order, one warp walking the peers.
+// Accumulation is exact (R#17): each fp16 scale is an integer multiple of
+// 2^-24.  When the chunk's nonzero scales span a small enough exponent range
+// (always, on real pseudo-gradients) the sum of R of them fits one int32 after
+// a common exact right shift — one shared atomic per entry, read back and
+// re-zeroed by one atomicExch; otherwise the value is split hi*2^20 + lo over
+// two int32 arrays as in aggregate.cu.  Either way the exact sum times the
+// exact 2^(sh-24) * invR is one fp64 rounding, then one fp32 rounding: the
+// oracle's (float)(acc * invR).  fma(-alpha, +0, theta) == theta for every
+// theta, so the dense pass needs no special case.  Weighted mode (median-norm
+// weights): fp64 in canonical peer order, one warp walking the peers.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -75,7 +78,10 @@ struct PipeSmem {
   __host__ __device__ static size_t off_desc(int R, int k, int RW) {
     return off_rec(R, k) + 2 * sizeof(uint32_t) * rec_buf_words(R, RW);
   }
-  __host__ __device__ static size_t bytes(int R, int k, int RW) { return off_desc(R, k, RW) + 4 * 16; }
+  // per-record scale table int4[R] and the chunk's scale-exponent range int2[2] (by buffer)
+  __host__ __device__ static size_t off_tab(int R, int k, int RW) { return off_desc(R, k, RW) + 4 * 16; }
+  __host__ __device__ static size_t off_erange(int R, int k, int RW) { return off_tab(R, k, RW) + 16 * R; }
+  __host__ __device__ static size_t bytes(int R, int k, int RW) { return off_erange(R, k, RW) + 16; }
 };
 
 #ifndef SLC_AGG_MINB
@@ -141,8 +147,7 @@ __device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int
 
 // all R records of chunk c -> srec (cp.async, 4 B each; records are 4-B aligned)
 template <int NT>
-__device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint32_t* srec, int t) {
-  const int RW = a.g.rec_words;
+__device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint32_t* srec, int t, int RW) {
   const int lane = t & 31, warp = t >> 5;
   for (int r = warp; r < a.R; r += NT / 32) {
     const uint32_t* rec = a.rec[r] + c * RW;
@@ -150,7 +155,9 @@ __device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint3
   }
 }
 
-template <int C, bool BF16, int MODE>
+// KC = 64: the default geometry (k = 64, 12-bit indices) with compile-time
+// record layout; KC = 0: any geometry, read from the arguments
+template <int C, bool BF16, int MODE, int KC>
 struct Pipe {
   using K = PipeCfg<C>;
   static constexpr int NT = K::NT;
@@ -166,19 +173,22 @@ struct Pipe {
   int64_t n, G;
   int64_t c;
   int4* ring;  // descriptors (first 16 B) of chunks c, c+G, c+2G, c+3G: slot = step & 3
+  int4* tab;   // per record: F(S_lo) lo/hi words, F(S_hi) lo/hi words; bit 31 of a hi word = non-finite
+  int2* erange;  // [buf]: min / max fp16 exponent field of the chunk's nonzero finite scales
   int it;      // step counter
   int buf;
   bool bad;
 
   // one chunk: `cur` holds chunk c's theta, `nxt` receives chunk c+G's
   __device__ __forceinline__ bool step(float (&cur)[16], float (&nxt)[16]) {
+    const int RWc = KC ? (KC * 12 + 31) / 32 + (2 * KC + 31) / 32 + 1 : a.g.rec_words;
     const int64_t cn = c + G;
     const bool has_next = cn < n;
     // descriptors travel through shared memory by cp.async, three chunks ahead:
     // a register load would be consumed (uniform-register move) at once
     if (has_next) {
       if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(ring[(it + 1) & 3]), t, nxt);
-      issue_records<NT>(a, cn, srec0 + (buf ^ 1) * bufw, t);
+      issue_records<NT>(a, cn, srec0 + (buf ^ 1) * bufw, t, RWc);
     }
     if (t == 0 && cn + 2 * G < n) cp_async16(&ring[(it + 3) & 3], a.chunks + cn + 2 * G);
     cp_async_commit();
@@ -186,29 +196,140 @@ struct Pipe {
 
     const uint32_t* srec = srec0 + buf * bufw;
     const int len = d0.len;
-    const int k_eff = max(1, (a.g.k * len) / C);
-    const int RW = a.g.rec_words, IW = a.g.idx_words, ib = a.g.ib;
+    const int kk = KC ? KC : a.g.k;
+    const int ib = KC ? 12 : a.g.ib;
+    const int IW = KC ? (KC * 12 + 31) / 32 : a.g.idx_words;
+    const int RW = RWc;
+    const int k_eff = max(1, (kk * len) / C);
     const int total = a.R * k_eff;
     cp_async_wait1();
-    __syncthreads();  // chunk c's records visible; previous chunk's passes done
+    if (!a.weighted && (t & 31) == (RW - 1) % 32) {
+      // this lane copied the scale word of records r = warp, warp + NW, ... (issue_records),
+      // so it may read them without a barrier: F = fp16 scale as a multiple of 2^-24
+      int emin = 31, emax = 0;
+      for (int r = t >> 5; r < a.R; r += NT / 32) {
+        const uint32_t sw = srec[r * RW + RW - 1];
+        uint32_t fw[4];
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          const uint32_t h = (sw >> (16 * b)) & 0xFFFFu;
+          const int e = (int)((h >> 10) & 0x1Fu);
+          const unsigned long long f = (unsigned long long)f16_fixed24(h);
+          fw[2 * b] = (uint32_t)f;
+          fw[2 * b + 1] = (uint32_t)(f >> 32) | (e == 31 ? 0x80000000u : 0u);
+          if ((h & 0x7FFFu) != 0 && e < 31) {
+            emin = min(emin, max(1, e));
+            emax = max(emax, max(1, e));
+          }
+        }
+        tab[r] = make_int4((int)fw[0], (int)fw[1], (int)fw[2], (int)fw[3]);
+      }
+      if (emin <= emax) {
+        atomicMin(&erange[buf].x, emin);
+        atomicMax(&erange[buf].y, emax);
+      }
+    }
+    __syncthreads();  // chunk c's records and scale table visible; previous chunk's passes done
 
-    if (!a.weighted) {
-      // pass 1: every entry into the exact accumulator; remember its position
-      for (int s = t; s < total; s += NT) {
-        const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
-        const int j = s - r * k_eff;
+    // Per chunk, one of three accumulators (CTA-uniform choice):
+    //  FAST  unit weights and every nonzero scale of the chunk within a
+    //        2^(20 - ceil(log2 R)) range: each decoded value F * 2^-24 is
+    //        F >> sh exactly (sh = min exponent - 1), and any sum of R of them
+    //        fits an int32: one native atomic per entry, read back and
+    //        re-zeroed by atomicExch
+    //  WIDE  unit weights otherwise: the R#17 hi*2^20 + lo split over two int32
+    //        arrays (acc, acc + C)
+    //  W     weights: fp64 in canonical peer order (one warp)
+    int mode;  // 0 FAST, 1 WIDE, 2 W
+    int sh = 0;
+    if (a.weighted) {
+      mode = 2;
+    } else {
+      const int2 er = erange[buf];
+      const int rbits = a.R > 1 ? 32 - __clz(a.R - 1) : 0;  // ceil(log2 R)
+      if (er.x > er.y || er.y - er.x + 11 + rbits <= 31) {
+        mode = 0;
+        sh = er.x > er.y ? 0 : er.x - 1;
+      } else {
+        mode = 1;
+      }
+    }
+    int* acc32 = reinterpret_cast<int*>(acc);
+
+    if (mode == 0 && k_eff == kk && (kk & 31) == 0) {
+      // pass 1, FAST, full chunk: warp w takes 32-slot units (record r, slots
+      // 32h..32h+31) with lane-constant bit offsets
+      const int KW = kk >> 5, lane = t & 31;
+      const int wl = (ib * lane) >> 5, shl = (ib * lane) & 31;
+      const int cw = IW + (lane >> 4), csh = 2 * (lane & 15);
+      const uint32_t imask = (1u << ib) - 1u;
+      const bool check_p = (1 << ib) > len;
+      for (int u = t >> 5; u < a.R * KW; u += NT / 32) {
+        const int r = u / KW;
+        const int h = u - r * KW;
         const uint32_t* rec = srec + r * RW;
-        uint32_t p = rec_index(rec, j, ib);
-        const uint32_t code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
-        const uint32_t sw = rec[RW - 1];
-        const uint32_t h = (code & 2u) ? (sw >> 16) : (sw & 0xFFFFu);
-        const long long f = f16_fixed24(h);
-        int lo = (int)(f & 0xFFFFF), hi = (int)(f >> 20);
-        if (code & 1u) { lo = -lo; hi = -hi; }
-        if ((int)p >= len || ((h >> 10) & 0x1Fu) == 0x1Fu) { bad = true; p = 0; lo = 0; hi = 0; }
+        uint32_t p = __funnelshift_r(rec[ib * h + wl], rec[ib * h + wl + 1], shl) & imask;
+        const uint32_t code = (rec[cw + 2 * h] >> csh) & 3u;
+        const int4 tb = tab[r];
+        const bool hb = (code & 2u) != 0;
+        const uint32_t flo = (uint32_t)(hb ? tb.z : tb.x), fhi = (uint32_t)(hb ? tb.w : tb.y);
+        int v = (int)__funnelshift_r(flo, fhi, sh);  // F >> sh, exact
+        bool ok = (fhi >> 31) == 0;
+        if (check_p) ok = ok && (int)p < len;
+        if (!ok) {
+          p = 0;
+          v = 0;
+          bad = true;
+        }
+        if (code & 1u) v = -v;
+        spos[r * kk + 32 * h + lane] = (uint16_t)p;
+        atomicAdd(&acc32[p], v);
+      }
+    } else if (mode < 2) {
+      // pass 1: every entry into the exact accumulator; remember its position.
+      // Full chunks: warp w takes 32-slot units (record r, slots 32h..32h+31)
+      // with lane-constant bit offsets; partial chunks walk entries.
+      const bool full = k_eff == kk && (k_eff & 31) == 0;
+      const int KW = k_eff >> 5, lane = t & 31;
+      const int wl = (ib * lane) >> 5, shl = (ib * lane) & 31;
+      const uint32_t imask = (1u << ib) - 1u;
+      const bool check_p = (1 << ib) > len;
+      const int n_iter = full ? a.R * KW : total;
+      for (int u = full ? (t >> 5) : t; u < n_iter; u += full ? NT / 32 : NT) {
+        int r, s;
+        uint32_t p, code;
+        if (full) {
+          r = KW == 2 ? (u >> 1) : u / KW;
+          const int h = u - r * KW;
+          const uint32_t* rec = srec + r * RW;
+          p = __funnelshift_r(rec[ib * h + wl], rec[ib * h + wl + 1], shl) & imask;
+          code = (rec[IW + 2 * h + (lane >> 4)] >> (2 * (lane & 15))) & 3u;
+          s = r * k_eff + 32 * h + lane;
+        } else {
+          s = u;
+          r = s / k_eff;
+          const int j = s - r * k_eff;
+          const uint32_t* rec = srec + r * RW;
+          p = rec_index(rec, j, ib);
+          code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
+        }
+        const int4 tb = tab[r];
+        const uint32_t flo = (uint32_t)((code & 2u) ? tb.z : tb.x);
+        const uint32_t fhi = (uint32_t)((code & 2u) ? tb.w : tb.y);
+        const bool ok = !(fhi >> 31) && !(check_p && (int)p >= len);
+        bad |= !ok;
+        if (!ok) p = 0;
         spos[s] = (uint16_t)p;
-        atomicAdd(&acc[p].x, lo);
-        atomicAdd(&acc[p].y, hi);
+        if (mode == 0) {
+          int v = ok ? (int)__funnelshift_r(flo, fhi, sh) : 0;  // F >> sh, exact
+          if (code & 1u) v = -v;
+          atomicAdd(&acc32[p], v);
+        } else {
+          int lo = ok ? (int)(flo & 0xFFFFFu) : 0, hi = ok ? (int)__funnelshift_r(flo, fhi, 20) : 0;
+          if (code & 1u) { lo = -lo; hi = -hi; }
+          atomicAdd(&acc32[p], lo);
+          atomicAdd(&acc32[C + p], hi);
+        }
       }
     } else {
       for (int s = t; s < total; s += NT) {
@@ -235,22 +356,32 @@ struct Pipe {
       }
     }
     __syncthreads();  // scatter complete
+    if (t == 0) erange[buf] = make_int2(31, 0);  // read by every thread before the barrier above
 
-    // pass 2: Delta only at touched positions (duplicates write the same value)
+    // pass 2: Delta only at touched positions; untouched dlt stay +0.  The
+    // oracle's Delta = (float)(acc * invR) with acc = V * 2^(sh-24) exactly,
+    // and 2^(sh-24) * invR is exact, so one fp64 product and one fp32 rounding.
     const double invR = a.invR;
-    const double c24 = invR * 0x1p-24;  // exact (power-of-two scaling)
-    for (int s = t; s < total; s += NT) {
-      const int p = spos[s];
-      const int2 v = acc[p];
-      float d;
-      if (a.weighted) {
-        d = __double2float_rn(__dmul_rn(__hiloint2double(v.y, v.x), invR));
-      } else {
-        // exact: hi*2^20 + lo (|.| < 2^53) is representable; one rounding in the product
-        const double sd = __fma_rn((double)v.y, 0x1p20, (double)v.x);
-        d = sd == 0.0 ? 0.0f : __double2float_rn(__dmul_rn(sd, c24));
+    if (mode == 0) {
+      const double cs = __dmul_rn(invR, __longlong_as_double((long long)(1023 + sh - 24) << 52));  // exact
+      for (int s = t; s < total; s += NT) {
+        const int p = spos[s];
+        const int v = atomicExch(&acc32[p], 0);  // exactly one entry of p sees the sum
+        if (v != 0) dlt[p] = __double2float_rn(__dmul_rn((double)v, cs));
       }
-      dlt[p] = d;
+    } else if (mode == 1) {
+      const double c24 = invR * 0x1p-24;
+      for (int s = t; s < total; s += NT) {
+        const int p = spos[s];
+        // exact: hi*2^20 + lo (|.| < 2^53) is representable; duplicates write the same value
+        const double sd = __fma_rn((double)acc32[C + p], 0x1p20, (double)acc32[p]);
+        dlt[p] = sd == 0.0 ? 0.0f : __double2float_rn(__dmul_rn(sd, c24));
+      }
+    } else {
+      for (int s = t; s < total; s += NT) {
+        const int p = spos[s];
+        dlt[p] = __double2float_rn(__dmul_rn(accd[p], invR));
+      }
     }
     __syncthreads();  // Delta complete
 
@@ -295,8 +426,17 @@ struct Pipe {
         }
       }
     }
-    // the accumulator is re-zeroed where it was touched (the next scatter follows a barrier)
-    for (int s = t; s < total; s += NT) acc[spos[s]] = make_int2(0, 0);
+    // WIDE / W: the accumulator is re-zeroed where it was touched (the next
+    // scatter follows a barrier); FAST re-zeroed it in pass 2
+    if (mode == 1) {
+      for (int s = t; s < total; s += NT) {
+        const int p = spos[s];
+        acc32[p] = 0;
+        acc32[C + p] = 0;
+      }
+    } else if (mode == 2) {
+      for (int s = t; s < total; s += NT) accd[spos[s]] = 0.0;
+    }
 
     c = cn;
     it++;
@@ -305,13 +445,13 @@ struct Pipe {
   }
 };
 
-template <int C, bool BF16, int MODE>
+template <int C, bool BF16, int MODE, int KC>
 __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pipe_kernel(const AggArgs a) {
   using S = PipeSmem<C>;
   constexpr int NT = PipeCfg<C>::NT;
   extern __shared__ __align__(16) unsigned char smem[];
   const int t = threadIdx.x;
-  Pipe<C, BF16, MODE> P{a};
+  Pipe<C, BF16, MODE, KC> P{a};
   P.acc = reinterpret_cast<int2*>(smem + S::off_acc);
   P.accd = reinterpret_cast<double*>(smem + S::off_acc);
   P.dlt = reinterpret_cast<float*>(smem + S::off_dlt);
@@ -326,17 +466,20 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   P.it = 0;
   P.bad = false;
   P.ring = reinterpret_cast<int4*>(smem + S::off_desc(a.R, a.g.k, a.g.rec_words));
+  P.tab = reinterpret_cast<int4*>(smem + S::off_tab(a.R, a.g.k, a.g.rec_words));
+  P.erange = reinterpret_cast<int2*>(smem + S::off_erange(a.R, a.g.k, a.g.rec_words));
   if (P.c >= P.n) return;
 
   for (int i = t; i < C / 2; i += NT) reinterpret_cast<int4*>(P.acc)[i] = make_int4(0, 0, 0, 0);
   for (int i = t; i < C / 4; i += NT) reinterpret_cast<float4*>(P.dlt)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (t < 2) P.srec0[t * P.bufw + a.R * a.g.rec_words] = 0u;  // rec_index may read one word past the last record
 
+  if (t < 2) P.erange[t] = make_int2(31, 0);
   if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
   __syncthreads();
   float thA[16], thB[16];
   if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(P.ring[0]), t, thA);
-  issue_records<NT>(a, P.c, P.srec0, t);
+  issue_records<NT>(a, P.c, P.srec0, t, a.g.rec_words);
   cp_async_commit();
 
   for (;;) {
@@ -349,7 +492,7 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
 template <int C, bool BF16, int MODE>
 cudaError_t launch_pipe(const AggArgs& a, cudaStream_t s) {
   if (a.R > kMaxPeers) return cudaErrorInvalidValue;
-  auto kern = agg_pipe_kernel<C, BF16, MODE>;
+  auto kern = (a.g.k == 64 && a.g.ib == 12) ? agg_pipe_kernel<C, BF16, MODE, 64> : agg_pipe_kernel<C, BF16, MODE, 0>;
   const size_t smem = PipeSmem<C>::bytes(a.R, a.g.k, a.g.rec_words);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

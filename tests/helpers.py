@@ -87,3 +87,57 @@ def seg_view(buf, s):
 def bits(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x)
     return x.view(np.uint16 if x.dtype.itemsize == 2 else np.uint32)
+
+
+def shard_chunk_lengths(plan, g=None):
+    """Positions per chunk of the shard, in shard chunk order."""
+    g = g or oracle.geom(plan.geom.block, plan.geom.k, plan.geom.index_bits)
+    C = plan.geom.chunk
+    out = []
+    for s in plan.segments:
+        shape = seg_shape(s)
+        nc = oracle.tensor_chunks(shape, g)
+        if oracle.is_blocked(shape, g):
+            out += [C] * nc
+        else:
+            n = int(np.prod(shape))
+            out += [min(C, n - c * C) for c in range(nc)]
+    return out
+
+
+def pack_record(pos, codes, s_lo_bits, s_hi_bits, k, ib):
+    """One record in the R#6 layout: slot j's index at stream
+    bits [ib*j, ib*j+ib), code bits 2j (sign) / 2j+1 (bucket) of the code
+    stream, last word s_lo | s_hi << 16; unused slots zero."""
+    iw = (k * ib + 31) // 32
+    cw = (2 * k + 31) // 32
+    words = np.zeros(iw + cw + 1, np.uint64)
+    for j, p in enumerate(pos):
+        b = ib * j
+        words[b // 32] |= np.uint64((int(p) << (b % 32)) & 0xFFFFFFFF)
+        if b % 32 + ib > 32:
+            words[b // 32 + 1] |= np.uint64(int(p) >> (32 - b % 32))
+        words[iw + (2 * j) // 32] |= np.uint64(int(codes[j]) << ((2 * j) % 32))
+    words[-1] = np.uint64(int(s_lo_bits) | (int(s_hi_bits) << 16))
+    return words.astype(np.uint32)
+
+
+def craft_records(plan, rng, exp_lo, exp_hi, zero_frac=0.05):
+    """A random but well-formed payload for the shard: per chunk k_eff distinct
+    ascending positions, random 2-bit codes and two fp16 scales whose exponent
+    fields are uniform in [exp_lo, exp_hi] (0 = subnormal), some zero."""
+    g = oracle.geom(plan.geom.block, plan.geom.k, plan.geom.index_bits)
+    k, ib = plan.geom.k, plan.geom.index_bits
+    out = []
+    for n in shard_chunk_lengths(plan, g):
+        ke = oracle.effective_k(n, g)
+        pos = np.sort(rng.choice(n, ke, replace=False))
+        codes = rng.integers(0, 4, ke)
+        sc = []
+        for _ in range(2):
+            if rng.random() < zero_frac:
+                sc.append(0)
+            else:
+                sc.append((int(rng.integers(exp_lo, exp_hi + 1)) << 10) | int(rng.integers(0, 1024)))
+        out.append(pack_record(pos, codes, sc[0], sc[1], k, ib))
+    return np.concatenate(out) if out else np.zeros(0, np.uint32)

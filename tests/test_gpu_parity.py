@@ -8,7 +8,8 @@ import pytest
 
 import oracle
 import slcgen
-from helpers import (bits, make_device_inputs, oracle_compress_shard, oracle_update_shard, seg_view)
+from helpers import (bits, craft_records, host_segment, make_device_inputs, oracle_compress_shard,
+                     oracle_update_shard, seg_view)
 from slcgen import layouts
 
 pytestmark = pytest.mark.gpu
@@ -96,6 +97,35 @@ def test_aggregate_update_parity(R, dtype, agg_kernel):
             fu, un = fu.view(torch.int16), un.view(torch.int16)
         assert np.array_equal(bits(fu.numpy()), tb)
         assert np.array_equal(bits(un.numpy()), tb)
+
+
+@pytest.mark.parametrize("R", [1, 2, 20, 64])
+@pytest.mark.parametrize("exps", [(4, 9), (0, 30), (1, 16)])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_aggregate_crafted_records(R, exps, dtype, agg_kernel):
+    """Decode / aggregate / update on random well-formed payloads whose fp16
+    scales span a chosen exponent range: (4, 9) keeps every chunk on the
+    single-int32 accumulator, (0, 30) (subnormal to 2^15) forces the wide
+    one, (1, 16) mixes both per chunk and R."""
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout, dtype=dtype)
+    rng = np.random.default_rng(1000 * R + exps[1])
+    theta, _, _ = make_device_inputs(plan, layout, 21, 0, dtype)
+    thetas = [host_segment(layout, s, slcgen.WHAT_THETA, 21, 0, dtype) for s in plan.segments]
+    ref_recs = [craft_records(plan, rng, *exps) for _ in range(R)]
+    recs = [torch.from_numpy(r.view(np.uint8).copy()).to(DEV) for r in ref_recs]
+    agg = torch.zeros(plan.shard_elems, dtype=torch.float32, device=DEV)
+    plan.decode_aggregate(recs, agg)
+    for s, d in zip(plan.segments, oracle_update_shard(plan, thetas, ref_recs, 1.0, only_delta=True)):
+        assert np.array_equal(bits(seg_view(agg, s).cpu().numpy()), bits(d))
+    alpha = 0.65
+    plan.outer_update(theta, alpha, records=recs)
+    assert plan.get_status() == slc.OK
+    for s, t in zip(plan.segments, oracle_update_shard(plan, thetas, ref_recs, alpha)):
+        got = seg_view(theta, s).cpu()
+        if dtype == "bf16":
+            got = got.view(torch.int16)
+        assert np.array_equal(bits(got.numpy()), bits(t))
 
 
 def test_permutation_invariance_and_weights(agg_kernel):
