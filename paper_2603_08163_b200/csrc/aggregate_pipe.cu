@@ -145,13 +145,41 @@ __device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int
   }
 }
 
-// all R records of chunk c -> srec (cp.async, 4 B each; records are 4-B aligned)
-template <int NT>
+// Slot of record r in a shared-memory record buffer: SR words (32 for the
+// compile-time layout, else RW).  Default layout (KC = 64, RW = 29 words =
+// 116 B): thread i = 8r + q copies record r — as eight 16-B pieces of the
+// 16-B-aligned 128-B window holding it ("wide"; the record then starts
+// o = (29c) & 3 words into the slot) when every record buffer is 16-B aligned
+// and the window stays inside the buffer (not the last chunk), else as 4-B
+// words w with w % 8 == (q + 5) % 8.  Either way thread 8r + 7 copies the
+// scale word (word 28), so it can read it after its own cp.async wait.
+template <int KC>
+__device__ __forceinline__ bool wide_window(const AggArgs& a, int64_t c) {
+  return KC == 64 && a.rec_al16 && c + 1 < a.n_chunks;
+}
+
+template <int NT, int KC>
 __device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint32_t* srec, int t, int RW) {
-  const int lane = t & 31, warp = t >> 5;
-  for (int r = warp; r < a.R; r += NT / 32) {
-    const uint32_t* rec = a.rec[r] + c * RW;
-    for (int w = lane; w < RW; w += 32) cp_async4(srec + r * RW + w, rec + w);
+  if (KC == 64) {
+    if (wide_window<KC>(a, c)) {
+      const int64_t wstart = (c * RW * 4) & ~(int64_t)15;
+      for (int i = t; i < a.R * 8; i += NT) {
+        const int r = i >> 3, q = i & 7;
+        cp_async16(srec + r * 32 + q * 4, reinterpret_cast<const char*>(a.rec[r]) + wstart + 16 * q);
+      }
+    } else {
+      for (int i = t; i < a.R * 8; i += NT) {
+        const int r = i >> 3, q = i & 7;
+        const uint32_t* rec = a.rec[r] + c * RW;
+        for (int w = (q + 5) & 7; w < RW; w += 8) cp_async4(srec + r * 32 + w, rec + w);
+      }
+    }
+  } else {
+    const int lane = t & 31, warp = t >> 5;
+    for (int r = warp; r < a.R; r += NT / 32) {
+      const uint32_t* rec = a.rec[r] + c * RW;
+      for (int w = lane; w < RW; w += 32) cp_async4(srec + r * RW + w, rec + w);
+    }
   }
 }
 
@@ -188,13 +216,14 @@ struct Pipe {
     // a register load would be consumed (uniform-register move) at once
     if (has_next) {
       if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(ring[(it + 1) & 3]), t, nxt);
-      issue_records<NT>(a, cn, srec0 + (buf ^ 1) * bufw, t, RWc);
+      issue_records<NT, KC>(a, cn, srec0 + (buf ^ 1) * bufw, t, RWc);
     }
     if (t == 0 && cn + 2 * G < n) cp_async16(&ring[(it + 3) & 3], a.chunks + cn + 2 * G);
     cp_async_commit();
     const Desc d0 = unpack_desc(ring[it & 3]);
 
-    const uint32_t* srec = srec0 + buf * bufw;
+    const int SR = KC ? 32 : RWc;  // slot words
+    const uint32_t* srec = srec0 + buf * bufw + (wide_window<KC>(a, c) ? (int)((29 * c) & 3) : 0);
     const int len = d0.len;
     const int kk = KC ? KC : a.g.k;
     const int ib = KC ? 12 : a.g.ib;
@@ -203,12 +232,13 @@ struct Pipe {
     const int k_eff = max(1, (kk * len) / C);
     const int total = a.R * k_eff;
     cp_async_wait1();
-    if (!a.weighted && (t & 31) == (RW - 1) % 32) {
-      // this lane copied the scale word of records r = warp, warp + NW, ... (issue_records),
-      // so it may read them without a barrier: F = fp16 scale as a multiple of 2^-24
+    const bool owner = KC ? (t & 7) == 7 : (t & 31) == (RW - 1) % 32;
+    if (!a.weighted && owner) {
+      // this thread copied the scale word of records r (issue_records), so it
+      // may read them without a barrier: F = fp16 scale as a multiple of 2^-24
       int emin = 31, emax = 0;
-      for (int r = t >> 5; r < a.R; r += NT / 32) {
-        const uint32_t sw = srec[r * RW + RW - 1];
+      for (int r = KC ? (t >> 3) : (t >> 5); r < a.R; r += KC ? NT / 8 : NT / 32) {
+        const uint32_t sw = srec[r * SR + RW - 1];
         uint32_t fw[4];
 #pragma unroll
         for (int b = 0; b < 2; b++) {
@@ -267,7 +297,7 @@ struct Pipe {
       for (int u = t >> 5; u < a.R * KW; u += NT / 32) {
         const int r = u / KW;
         const int h = u - r * KW;
-        const uint32_t* rec = srec + r * RW;
+        const uint32_t* rec = srec + r * SR;
         uint32_t p = __funnelshift_r(rec[ib * h + wl], rec[ib * h + wl + 1], shl) & imask;
         const uint32_t code = (rec[cw + 2 * h] >> csh) & 3u;
         const int4 tb = tab[r];
@@ -301,7 +331,7 @@ struct Pipe {
         if (full) {
           r = KW == 2 ? (u >> 1) : u / KW;
           const int h = u - r * KW;
-          const uint32_t* rec = srec + r * RW;
+          const uint32_t* rec = srec + r * SR;
           p = __funnelshift_r(rec[ib * h + wl], rec[ib * h + wl + 1], shl) & imask;
           code = (rec[IW + 2 * h + (lane >> 4)] >> (2 * (lane & 15))) & 3u;
           s = r * k_eff + 32 * h + lane;
@@ -309,7 +339,7 @@ struct Pipe {
           s = u;
           r = s / k_eff;
           const int j = s - r * k_eff;
-          const uint32_t* rec = srec + r * RW;
+          const uint32_t* rec = srec + r * SR;
           p = rec_index(rec, j, ib);
           code = (rec[IW + (j >> 4)] >> (2 * (j & 15))) & 3u;
         }
@@ -334,12 +364,12 @@ struct Pipe {
     } else {
       for (int s = t; s < total; s += NT) {
         const int r = k_eff == 64 ? (s >> 6) : s / k_eff;
-        const uint32_t p = rec_index(srec + r * RW, s - r * k_eff, ib);
+        const uint32_t p = rec_index(srec + r * SR, s - r * k_eff, ib);
         spos[s] = (int)p < len ? (uint16_t)p : (uint16_t)0;
       }
       if (t < 32) {
         for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
-          const uint32_t* rec = srec + i * RW;
+          const uint32_t* rec = srec + i * SR;
           const double w = (double)a.w[i];
           const uint32_t sw = rec[RW - 1];
           for (int j = t; j < k_eff; j += 32) {
@@ -456,8 +486,9 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   P.accd = reinterpret_cast<double*>(smem + S::off_acc);
   P.dlt = reinterpret_cast<float*>(smem + S::off_dlt);
   P.spos = reinterpret_cast<uint16_t*>(smem + S::off_pos);
+  const int SR = KC ? 32 : a.g.rec_words;
   P.srec0 = reinterpret_cast<uint32_t*>(smem + S::off_rec(a.R, a.g.k));
-  P.bufw = rec_buf_words(a.R, a.g.rec_words);
+  P.bufw = rec_buf_words(a.R, SR);
   P.t = t;
   P.n = a.n_chunks;
   P.G = gridDim.x;
@@ -465,21 +496,21 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   P.buf = 0;
   P.it = 0;
   P.bad = false;
-  P.ring = reinterpret_cast<int4*>(smem + S::off_desc(a.R, a.g.k, a.g.rec_words));
-  P.tab = reinterpret_cast<int4*>(smem + S::off_tab(a.R, a.g.k, a.g.rec_words));
-  P.erange = reinterpret_cast<int2*>(smem + S::off_erange(a.R, a.g.k, a.g.rec_words));
+  P.ring = reinterpret_cast<int4*>(smem + S::off_desc(a.R, a.g.k, SR));
+  P.tab = reinterpret_cast<int4*>(smem + S::off_tab(a.R, a.g.k, SR));
+  P.erange = reinterpret_cast<int2*>(smem + S::off_erange(a.R, a.g.k, SR));
   if (P.c >= P.n) return;
 
   for (int i = t; i < C / 2; i += NT) reinterpret_cast<int4*>(P.acc)[i] = make_int4(0, 0, 0, 0);
   for (int i = t; i < C / 4; i += NT) reinterpret_cast<float4*>(P.dlt)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  if (t < 2) P.srec0[t * P.bufw + a.R * a.g.rec_words] = 0u;  // rec_index may read one word past the last record
+  if (t < 2) P.srec0[t * P.bufw + a.R * SR] = 0u;  // rec_index may read one word past the last record
 
   if (t < 2) P.erange[t] = make_int2(31, 0);
   if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
   __syncthreads();
   float thA[16], thB[16];
   if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(P.ring[0]), t, thA);
-  issue_records<NT>(a, P.c, P.srec0, t, a.g.rec_words);
+  issue_records<NT, KC>(a, P.c, P.srec0, t, a.g.rec_words);
   cp_async_commit();
 
   for (;;) {
@@ -492,8 +523,9 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
 template <int C, bool BF16, int MODE>
 cudaError_t launch_pipe(const AggArgs& a, cudaStream_t s) {
   if (a.R > kMaxPeers) return cudaErrorInvalidValue;
-  auto kern = (a.g.k == 64 && a.g.ib == 12) ? agg_pipe_kernel<C, BF16, MODE, 64> : agg_pipe_kernel<C, BF16, MODE, 0>;
-  const size_t smem = PipeSmem<C>::bytes(a.R, a.g.k, a.g.rec_words);
+  const bool fixed = a.g.k == 64 && a.g.ib == 12;
+  auto kern = fixed ? agg_pipe_kernel<C, BF16, MODE, 64> : agg_pipe_kernel<C, BF16, MODE, 0>;
+  const size_t smem = PipeSmem<C>::bytes(a.R, a.g.k, fixed ? 32 : a.g.rec_words);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -513,8 +545,8 @@ cudaError_t launch_pipe(const AggArgs& a, cudaStream_t s) {
 
 bool aggregate_pipe_supported(const AggArgs& a) {
   if (a.g.C != 1024 && a.g.C != 4096) return false;
-  const size_t smem = a.g.C == 1024 ? PipeSmem<1024>::bytes(a.R, a.g.k, a.g.rec_words)
-                                    : PipeSmem<4096>::bytes(a.R, a.g.k, a.g.rec_words);
+  const int SR = (a.g.k == 64 && a.g.ib == 12) ? 32 : a.g.rec_words;
+  const size_t smem = a.g.C == 1024 ? PipeSmem<1024>::bytes(a.R, a.g.k, SR) : PipeSmem<4096>::bytes(a.R, a.g.k, SR);
   return smem <= 200 * 1024;  // leaves room for 1 CTA per SM with any driver reservation
 }
 

@@ -165,6 +165,7 @@ slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const*
   a.R = R;
   a.weighted = w != nullptr;
   a.invR = 1.0 / (double)R;
+  a.rec_al16 = 1;
   a.err = p->d_err;
   a.g = p->g;
   for (int i = 0; i < R; i++) {
@@ -172,6 +173,7 @@ slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const*
     if (!recs[r] && p->n_chunks > 0) return SLC_ERR_INVALID_ARGUMENT;
     if (((uintptr_t)recs[r]) & 3u) return SLC_ERR_INVALID_ARGUMENT;
     a.rec[i] = static_cast<const uint32_t*>(recs[r]);
+    if (((uintptr_t)recs[r]) & 15u) a.rec_al16 = 0;
     a.w[i] = w ? w[r] : 1.0f;
   }
   return SLC_OK;

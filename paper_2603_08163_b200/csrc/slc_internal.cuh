@@ -76,6 +76,7 @@ struct AggArgs {
   const uint32_t* rec[kMaxPeers];  // per peer: this shard's records
   float w[kMaxPeers];              // per peer weight (weighted mode only)
   int R;
+  int rec_al16;  // every rec[r] is 16-byte aligned (enables 16-B record copies)
   int weighted;
   int mode;
   float alpha;

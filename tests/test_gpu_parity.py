@@ -128,6 +128,29 @@ def test_aggregate_crafted_records(R, exps, dtype, agg_kernel):
         assert np.array_equal(bits(got.numpy()), bits(t))
 
 
+@pytest.mark.parametrize("R", [3, 20])
+@pytest.mark.parametrize("offset", [4, 8, 12])
+def test_aggregate_misaligned_record_buffers(R, offset, agg_kernel):
+    """Record buffers that are only 4-B aligned (the C ABI's requirement) take
+    the word-by-word staging path; results are unchanged."""
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout)
+    rng = np.random.default_rng(77 + R + offset)
+    theta, _, _ = make_device_inputs(plan, layout, 23, 0)
+    thetas = [host_segment(layout, s, slcgen.WHAT_THETA, 23, 0) for s in plan.segments]
+    ref_recs = [craft_records(plan, rng, 2, 12) for _ in range(R)]
+    recs = []
+    for r in ref_recs:
+        buf = torch.zeros(r.nbytes + 16, dtype=torch.uint8, device=DEV)
+        v = buf[offset:offset + r.nbytes]
+        v.copy_(torch.from_numpy(r.view(np.uint8).copy()))
+        recs.append(v)
+    plan.outer_update(theta, 1.0, records=recs)
+    assert plan.get_status() == slc.OK
+    for s, t in zip(plan.segments, oracle_update_shard(plan, thetas, ref_recs, 1.0)):
+        assert np.array_equal(bits(seg_view(theta, s).cpu().numpy()), bits(t))
+
+
 def test_permutation_invariance_and_weights(agg_kernel):
     layout = layouts.LAYOUTS["ragged"]
     plan = slc.Plan(layout)
