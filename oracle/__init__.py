@@ -297,3 +297,43 @@ def index_entropy_bound(C: int, k: int) -> float:
 
 def compression_ratio(C: int, k: int, dense_bits: int, wire_bits_per_value: int) -> float:
     return float(_load().slco_compression_ratio(C, k, dense_bits, wire_bits_per_value))
+
+
+# ---------------------------------------------------------------- median-norm (reading R#20)
+def payload_norm(chunks, g=None) -> float:
+    """||hatDelta_r||_2 of one peer's payload ("scaled relative to their
+    median norm"), by the plain definition: decode every chunk (record,
+    n_positions) and sum the squares of the decoded values.  Each value is an
+    fp16 scale with a sign, so its square is exact in binary64 and math.fsum
+    returns the correctly rounded sum of the exact squares; math.sqrt is
+    correctly rounded.  (Reading R#20: the norm of the transmitted, decoded
+    pseudo-gradient, computed per peer over the whole payload.)"""
+    import math
+    g = g or geom()
+    sq = []
+    for rec, n in chunks:
+        _, dq = decode_chunk(rec, n, g)
+        sq.extend(float(x) * float(x) for x in dq)
+    return math.sqrt(math.fsum(sq))
+
+
+def median_norm_weights(norms) -> np.ndarray:
+    """Per-peer weights of the median-norm normalisation:
+    m = lower median of the norms (S:283 design decision: lower median for
+    even counts); a peer with norm > 0 is rescaled to norm m, w_r = m / n_r
+    (binary64 division, then rounded to fp32: the weight enters Eq. 2 as an
+    fp32 factor); zero norms pass through (w = 1)."""
+    n = [float(x) for x in norms]
+    if not n:
+        raise ValueError("median_norm_weights: no peers")
+    m = sorted(n)[(len(n) - 1) // 2]
+    return np.array([np.float32(m / x) if x > 0 else np.float32(1.0) for x in n], np.float32)
+
+
+def median_normalize(deltas):
+    """SPEC S:280 median_normalize on dense deltas (test helper for the pins):
+    every delta with norm > 0 rescaled to the lower-median norm."""
+    import math
+    norms = [math.sqrt(math.fsum(float(v) * float(v) for v in np.asarray(d, np.float64).ravel())) for d in deltas]
+    m = sorted(norms)[(len(norms) - 1) // 2]
+    return [np.asarray(d, np.float64) * (m / nn) if nn > 0 else np.asarray(d, np.float64) for d, nn in zip(deltas, norms)]

@@ -459,3 +459,71 @@ def test_bf16_inputs_are_widened_exactly():
     st1, r1, e1 = oracle.compress_chunk(ab, lb, e, 0.95)
     st2, r2, e2 = oracle.compress_chunk(a.float().numpy(), l.float().numpy(), e, 0.95)
     assert st1 == st2 == 0 and (r1 == r2).all() and (e1.view(np.uint32) == e2.view(np.uint32)).all()
+
+
+# ---------------------------------------------------------------- median-norm (R#20)
+def test_median_normalize_spec_example_norms_1_2_4():
+    """norms [1, 2, 4] -> every output has norm 2 (rescale factors 2, 1, 0.5)."""
+    rng = np.random.default_rng(5)
+    base = [rng.normal(size=50) for _ in range(3)]
+    deltas = [b / np.linalg.norm(b) * s for b, s in zip(base, [1.0, 2.0, 4.0])]
+    out = oracle.median_normalize(deltas)
+    for o in out:
+        assert abs(np.linalg.norm(o) - 2.0) < 1e-12
+    w = oracle.median_norm_weights([1.0, 2.0, 4.0])
+    assert list(w) == [2.0, 1.0, 0.5]
+
+
+def test_median_norm_weights_properties():
+    # all equal -> unchanged (S:286); zero norms pass through; lower median for even counts (S:283)
+    assert list(oracle.median_norm_weights([3.0, 3.0, 3.0])) == [1.0, 1.0, 1.0]
+    assert list(oracle.median_norm_weights([0.0, 2.0, 2.0])) == [1.0, 1.0, 1.0]
+    assert list(oracle.median_norm_weights([1.0, 2.0, 4.0, 8.0])) == [2.0, 1.0, 0.5, 0.25]
+    # one adversarial peer (S:287): its contribution is bounded by the median
+    n = [1.0, 1.1, 0.9, 1e6]
+    w = oracle.median_norm_weights(n)
+    assert abs(float(w[3]) * 1e6 - 1.0) < 1e-6
+    # permutation invariance and scale equivariance (S:302): weights unchanged when
+    # every norm is scaled by a power of two
+    rng = np.random.default_rng(9)
+    n = list(rng.uniform(0.1, 5.0, 9))
+    w = oracle.median_norm_weights(n)
+    perm = rng.permutation(9)
+    assert np.array_equal(oracle.median_norm_weights([n[i] for i in perm]), w[perm])
+    assert np.array_equal(oracle.median_norm_weights([x * 8.0 for x in n]), w)
+
+
+def _f16_fraction(h):
+    from fractions import Fraction
+    e, m = (h >> 10) & 0x1F, h & 0x3FF
+    return Fraction(m, 1 << 24) if e == 0 else Fraction(1024 + m, 1 << 24) * (1 << (e - 1))
+
+
+def test_payload_norm_is_exact_sum_of_squares():
+    """payload_norm (decode + fsum) equals sqrt(RN(exact rational sum)) built
+    directly from the fp16 bit patterns and codes, on random payloads whose
+    scales span the whole fp16 range (subnormal to 2^15)."""
+    import math
+    from helpers import pack_record
+    g = oracle.geom()
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        chunks, exact = [], 0
+        for _ in range(int(rng.integers(1, 6))):
+            n = int(rng.choice([4096, 1000]))
+            ke = oracle.effective_k(n, g)
+            pos = np.sort(rng.choice(n, ke, replace=False))
+            codes = rng.integers(0, 4, ke)
+            sc = [(int(rng.integers(0, 31)) << 10) | int(rng.integers(0, 1024)) for _ in range(2)]
+            chunks.append((pack_record(pos, codes, sc[0], sc[1], 64, 12), n))
+            exact += sum(_f16_fraction(sc[(int(c) >> 1) & 1]) ** 2 for c in codes)
+        assert oracle.payload_norm(chunks, g) == math.sqrt(float(exact))
+
+
+def test_payload_norm_closed_form():
+    # one chunk, every slot in the hi bucket with scale S: ||.||^2 = k * S^2
+    from helpers import pack_record
+    g = oracle.geom()
+    S = 0x3C00  # 1.0 in fp16
+    rec = pack_record(np.arange(64) * 3, np.full(64, 2), 0, S, 64, 12)
+    assert oracle.payload_norm([(rec, 4096)], g) == 8.0
