@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run shard --shard-rank of an N-way FSDP sharding (one GPU's share of a larger job)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--median-norm", action="store_true",
+                    help="median-norm weights (P:101): exact payload norms + all-reduce + weighted fused update")
     return ap.parse_args()
 
 
@@ -214,6 +216,9 @@ def run_slc(args):
     peers = make_peer_records(plan, layout, shard, seed=0, n_peers=R - 1, first_peer=1, dtype=dtype)
     shard.reset()
     recs = [shard.records[:plan.payload_bytes]] + peers
+    mnorm = sdist.MedianNorm(plan, R, device=dev) if args.median_norm else None
+    hdrs = ([slc.make_header(plan, bytes([r + 1]) * 16, base_round=1) for r in range(R)]
+            if args.median_norm else None)
 
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -227,7 +232,11 @@ def run_slc(args):
             ev[i][1].record(stream)
         if gather is not None:
             gather.start(shard.records)
-        plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
+        if mnorm is not None:
+            w = mnorm(recs, hdrs=hdrs, stream=stream)
+            plan.outer_update(shard.theta, ALPHA, records=recs, hdrs=hdrs, weights_dev=w, stream=stream)
+        else:
+            plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
         if gather is not None:
             gather.wait()
         if i is not None:
@@ -313,9 +322,12 @@ def run_slc(args):
                      "algorithmic_bytes_per_launch": comp_bytes, "peak_source": peak_src},
         "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
                     "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (4 if args.median_norm else 2) * args.steps,
         "clocks": clk.summary(),
     }
+    if args.median_norm:
+        out["config"]["median_norm"] = ("P:101: exact payload norms (slc_payload_sqnorm) + int64 all-reduce + "
+                                        "lower-median weights on device + weighted fused update; in the timed step")
     if args.shard_of:
         out["config"]["shard"] = (f"rank {args.shard_rank} of {args.shard_of} ({n_local} params on this GPU); "
                                   "value = this shard's params / step time")

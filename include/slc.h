@@ -172,6 +172,39 @@ slc_status slc_outer_update(slc_plan* plan, void* theta_dev, const float* agg_de
                             const slc_payload_hdr* hdrs_host, const void* const* records_dev_host, int32_t R,
                             const float* weights_host, float alpha, void* stream);
 
+/* Median-norm normalisation ("Pseudo-gradient contributions are scaled
+ * relative to their median norm so that no single participant can dominate";
+ * reading R#20: every nonzero contribution rescaled to the
+ * lower-median norm; zero contributions pass through).  Three calls, no host
+ * synchronisation:
+ *
+ * 1. slc_payload_sqnorm: ||hatDelta_r||^2 of each peer's payload restricted to
+ *    this plan's shard, computed from the records alone and EXACT: an integer
+ *    in units of 2^-48, returned as four un-carried 32-bit limbs per peer,
+ *      sqnorm_dev[4r + i] (uint64, device, caller's peer order r = 0..R-1),
+ *      value = sum_i sqnorm_dev[4r + i] * 2^(32 i).
+ *    Limbs of several shards add exactly (an int64 sum, e.g. an NCCL
+ *    all-reduce over the ranks), so the result is independent of the sharding.
+ *    hdrs/records/R as for slc_decode_aggregate.  The call zeroes sqnorm_dev
+ *    first.  Latches INVALID_DATA on a non-finite scale.
+ * 2. slc_median_norm_weights: from the (summed) limbs, n_r = sqrt(RN64(value *
+ *    2^-48)) (IEEE), m = lower median of the n_r, weights_dev[r] =
+ *    RN32(m / n_r) for n_r > 0 else 1 (fp32, device, caller's order);
+ *    norms_dev[r] = n_r (fp64, device) unless NULL.  1 <= R <= 256.
+ * 3. slc_decode_aggregate_wdev / slc_outer_update_wdev: as slc_decode_aggregate /
+ *    slc_outer_update (fused) with weights read from weights_dev (device, the
+ *    caller's peer order) — fp64 sum in ascending peer-id order. */
+slc_status slc_payload_sqnorm(slc_plan* plan, const slc_payload_hdr* hdrs_host, const void* const* records_dev_host,
+                              int32_t R, uint64_t* sqnorm_dev, void* stream);
+slc_status slc_median_norm_weights(slc_plan* plan, int32_t R, const uint64_t* sqnorm_dev, float* weights_dev,
+                                   double* norms_dev, void* stream);
+slc_status slc_decode_aggregate_wdev(slc_plan* plan, const slc_payload_hdr* hdrs_host,
+                                     const void* const* records_dev_host, int32_t R, const float* weights_dev,
+                                     float* agg_dev, void* stream);
+slc_status slc_outer_update_wdev(slc_plan* plan, void* theta_dev, const slc_payload_hdr* hdrs_host,
+                                 const void* const* records_dev_host, int32_t R, const float* weights_dev,
+                                 float alpha, void* stream);
+
 /* Latched device-side status of the plan.  synchronize != 0: wait for the
  * plan's device, read and clear the device error word.  synchronize == 0:
  * return (and clear) what was already latched on the host. */

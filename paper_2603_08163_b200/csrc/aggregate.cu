@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(C / 16) aggregate_kernel(const AggArgs a) {
     } else if (t < 32) {
       for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
         const uint32_t* rec = staged ? srec + i * RW : a.rec[i] + chunk * RW;
-        const double w = (double)a.w[i];
+        const double w = peer_weight(a, i);
         const uint32_t sw = rec[RW - 1];
         for (int j = t; j < k_eff; j += 32) {
           const uint32_t p = rec_index(rec, j, ib);

@@ -370,7 +370,7 @@ struct Pipe {
       if (t < 32) {
         for (int i = 0; i < a.R; i++) {  // canonical peer order (host-sorted)
           const uint32_t* rec = srec + i * SR;
-          const double w = (double)a.w[i];
+          const double w = peer_weight(a, i);
           const uint32_t sw = rec[RW - 1];
           for (int j = t; j < k_eff; j += 32) {
             const uint32_t p = rec_index(rec, j, ib);

@@ -175,6 +175,7 @@ slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const*
     a.rec[i] = static_cast<const uint32_t*>(recs[r]);
     if (((uintptr_t)recs[r]) & 15u) a.rec_al16 = 0;
     a.w[i] = w ? w[r] : 1.0f;
+    a.worder[i] = (int16_t)r;
   }
   return SLC_OK;
 }
@@ -462,6 +463,63 @@ slc_status slc_outer_update(slc_plan* p, void* theta, const float* agg, const sl
   a.theta = theta;
   DeviceGuard guard(p->device);
   return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_decode_aggregate_wdev(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
+                                     const float* w_dev, float* agg, void* stream) {
+  if (!p || p->device < 0 || !w_dev) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  slc_status st = prep_agg(p, hdrs, recs, R, nullptr, a);
+  if (st != SLC_OK) return st;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!agg || !aligned16(agg)) return SLC_ERR_INVALID_ARGUMENT;
+  a.weighted = 1;
+  a.wdev = w_dev;
+  a.mode = slc::kAggOnly;
+  a.agg = agg;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_outer_update_wdev(slc_plan* p, void* theta, const slc_payload_hdr* hdrs, const void* const* recs,
+                                 int32_t R, const float* w_dev, float alpha, void* stream) {
+  if (!p || p->device < 0 || !w_dev) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  slc_status st = prep_agg(p, hdrs, recs, R, nullptr, a);
+  if (st != SLC_OK) return st;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!theta || !aligned16(theta)) return SLC_ERR_INVALID_ARGUMENT;
+  a.weighted = 1;
+  a.wdev = w_dev;
+  a.mode = slc::kFused;
+  a.alpha = alpha;
+  a.theta = theta;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_payload_sqnorm(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
+                              uint64_t* sqnorm_dev, void* stream) {
+  if (!p || p->device < 0 || !sqnorm_dev || (((uintptr_t)sqnorm_dev) & 7u)) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  slc_status st = prep_agg(p, hdrs, recs, R, nullptr, a);
+  if (st != SLC_OK) return st;
+  // caller's peer order (not canonical): limbs of peer r go to sqnorm_dev[4r..4r+3]
+  for (int r = 0; r < R; r++) a.rec[r] = static_cast<const uint32_t*>(recs[r]);
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_payload_sqnorm(a, reinterpret_cast<unsigned long long*>(sqnorm_dev),
+                                                static_cast<cudaStream_t>(stream)),
+                     p);
+}
+
+slc_status slc_median_norm_weights(slc_plan* p, int32_t R, const uint64_t* sqnorm_dev, float* weights_dev,
+                                   double* norms_dev, void* stream) {
+  if (!p || p->device < 0 || R < 1 || R > slc::kMaxPeers || !sqnorm_dev || !weights_dev)
+    return SLC_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_median_weights(reinterpret_cast<const unsigned long long*>(sqnorm_dev), R,
+                                                weights_dev, norms_dev, static_cast<cudaStream_t>(stream)),
+                     p);
 }
 
 slc_status slc_get_status(slc_plan* p, int32_t synchronize) {

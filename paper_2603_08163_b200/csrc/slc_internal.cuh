@@ -75,6 +75,8 @@ struct AggArgs {
   int64_t n_chunks;
   const uint32_t* rec[kMaxPeers];  // per peer: this shard's records
   float w[kMaxPeers];              // per peer weight (weighted mode only)
+  const float* wdev;               // weighted mode: device weights in the caller's peer order, or NULL (use w)
+  int16_t worder[kMaxPeers];       // canonical position i -> caller's peer index (for wdev)
   int R;
   int rec_al16;  // every rec[r] is 16-byte aligned (enables 16-B record copies)
   int weighted;
@@ -102,6 +104,16 @@ cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
 // persistent software-pipelined decode / fused update (C = 1024, 4096)
 cudaError_t launch_aggregate_pipe(const AggArgs& a, int param_bf16, cudaStream_t s);
 bool aggregate_pipe_supported(const AggArgs& a);
+// median-norm: exact per-peer squared norms as 4 un-carried 32-bit limbs per peer; weights
+cudaError_t launch_payload_sqnorm(const AggArgs& a, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_median_weights(const unsigned long long* limbs, int R, float* w, double* norms, cudaStream_t s);
+
+#ifdef __CUDACC__
+// weight of canonical peer i (weighted mode)
+__device__ __forceinline__ double peer_weight(const AggArgs& a, int i) {
+  return (double)(a.wdev ? __ldg(a.wdev + a.worder[i]) : a.w[i]);
+}
+#endif
 bool compress_supported(int C);
 
 }  // namespace slc

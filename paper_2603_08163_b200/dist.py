@@ -103,3 +103,33 @@ class PeerExchange:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         return [s[:self.g.sizes[rank]] for s in self.slices]
+
+
+class MedianNorm:
+    """Median-norm weights (reading R#20) for the R peers of one round,
+    identical on every rank: each rank computes the exact squared norms of its
+    shard of every peer's payload (slc_payload_sqnorm: four un-carried 32-bit
+    limbs per peer), one int64 all-reduce (SUM) adds the limbs exactly — the
+    only extra collective, 32*R bytes — and slc_median_norm_weights turns them
+    into weights on the device.  No host synchronisation."""
+
+    def __init__(self, plan: slc.Plan, n_peers: int, group=None, device=None):
+        self.plan = plan
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.limbs = torch.zeros((n_peers, 4), dtype=torch.int64, device=dev)
+        self.weights = torch.ones(n_peers, dtype=torch.float32, device=dev)
+        self.norms = torch.zeros(n_peers, dtype=torch.float64, device=dev)
+
+    def reduce_limbs(self, limbs: torch.Tensor) -> torch.Tensor:
+        """Exact cross-rank sum of the un-carried limbs (each < 2^63 for any realistic job)."""
+        if self.world > 1:
+            dist.all_reduce(limbs, op=dist.ReduceOp.SUM, group=self.group)
+        return limbs
+
+    def __call__(self, records: Sequence[torch.Tensor], hdrs=None, stream=None) -> torch.Tensor:
+        self.plan.payload_sqnorm(records, self.limbs, hdrs=hdrs, stream=stream)
+        self.reduce_limbs(self.limbs)
+        self.plan.median_norm_weights(self.limbs, self.weights, self.norms, stream=stream)
+        return self.weights

@@ -73,6 +73,10 @@ def _load():
         "slc_compress": (ctypes.c_int, [P, P, P, P, ctypes.c_float, P, P]),
         "slc_decode_aggregate": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
         "slc_outer_update": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
+        "slc_payload_sqnorm": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P]),
+        "slc_median_norm_weights": (ctypes.c_int, [P, ctypes.c_int32, P, P, P, P]),
+        "slc_decode_aggregate_wdev": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
+        "slc_outer_update_wdev": (ctypes.c_int, [P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
         "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -87,8 +91,9 @@ def _load():
 _lib = _load()
 
 EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_record_bytes", "slc_layout_digest",
-            "slc_compress", "slc_decode_aggregate", "slc_outer_update", "slc_get_status", "slc_plan_destroy",
-            "slc_status_string"]
+            "slc_compress", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
+            "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_get_status",
+            "slc_plan_destroy", "slc_status_string"]
 
 
 def status_string(s: int) -> str:
@@ -235,16 +240,39 @@ class Plan:
             w = (ctypes.c_float * R)(*[float(x) for x in weights])
         return R, ptrs, h, w
 
-    def decode_aggregate(self, records: Sequence, agg, hdrs=None, weights=None, stream=None) -> None:
-        """Eq. 2 line 1: agg[shard_elems] f32 <- (1/R) sum_r w_r decode(records[r])."""
+    def decode_aggregate(self, records: Sequence, agg, hdrs=None, weights=None, stream=None,
+                         weights_dev=None) -> None:
+        """Eq. 2 line 1: agg[shard_elems] f32 <- (1/R) sum_r w_r decode(records[r]).
+        weights: host floats; weights_dev: [R] f32 device tensor (e.g. median_norm_weights)."""
         R, ptrs, h, w = self._peer_args(records, hdrs, weights)
+        if weights_dev is not None:
+            _check(_lib.slc_decode_aggregate_wdev(self._h, h, ptrs, R, _dptr(weights_dev), _dptr(agg),
+                                                  _stream_ptr(stream)), "slc_decode_aggregate_wdev")
+            return
         _check(_lib.slc_decode_aggregate(self._h, h, ptrs, R, w, _dptr(agg), _stream_ptr(stream)),
                "slc_decode_aggregate")
 
+    # ---- median-norm normalisation (P:101, DESIGN.md R#20)
+    def payload_sqnorm(self, records: Sequence, out, hdrs=None, stream=None) -> None:
+        """out: [R, 4] int64 (uint64 limbs) device tensor <- exact ||hatDelta_r||^2 over this shard."""
+        R, ptrs, h, _ = self._peer_args(records, hdrs, None)
+        assert out.numel() >= 4 * R and out.element_size() == 8
+        _check(_lib.slc_payload_sqnorm(self._h, h, ptrs, R, _dptr(out), _stream_ptr(stream)), "slc_payload_sqnorm")
+
+    def median_norm_weights(self, sqnorm, weights, norms=None, stream=None) -> None:
+        """weights: [R] f32 device tensor <- lower-median / ||hatDelta_r|| from the (rank-summed) limbs."""
+        R = weights.numel()
+        _check(_lib.slc_median_norm_weights(self._h, R, _dptr(sqnorm), _dptr(weights), _dptr(norms),
+                                            _stream_ptr(stream)), "slc_median_norm_weights")
+
     def outer_update(self, theta, alpha: float = 1.0, agg=None, records: Optional[Sequence] = None, hdrs=None,
-                     weights=None, stream=None) -> None:
+                     weights=None, stream=None, weights_dev=None) -> None:
         """Eq. 2 line 2: theta <- theta - alpha * Delta; agg=None -> fused decode/aggregate/update."""
-        if agg is not None:
+        if weights_dev is not None:
+            R, ptrs, h, _ = self._peer_args(records, hdrs, None)
+            _check(_lib.slc_outer_update_wdev(self._h, _dptr(theta), h, ptrs, R, _dptr(weights_dev),
+                                              ctypes.c_float(alpha), _stream_ptr(stream)), "slc_outer_update_wdev")
+        elif agg is not None:
             _check(_lib.slc_outer_update(self._h, _dptr(theta), _dptr(agg), None, None, 0, None,
                                          ctypes.c_float(alpha), _stream_ptr(stream)), "slc_outer_update")
         else:

@@ -81,3 +81,62 @@ def test_gather_and_exchange_gloo(world, layout_name, n_peers):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(g and e for _, g, e in res), res
+
+
+def _median_worker(rank, world, port, q):
+    """Each rank holds the exact squared norms of its shard of R crafted payloads
+    as 32-bit limbs (host stand-in for slc_payload_sqnorm); MedianNorm's int64
+    all-reduce must reproduce the whole payloads' exact sums on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import __graft_entry__
+        __graft_entry__.build()
+        from fractions import Fraction
+
+        import oracle
+        from helpers import craft_records, shard_chunk_lengths
+        from paper_2603_08163_b200 import slc
+        from paper_2603_08163_b200.dist import MedianNorm
+        layout = layouts.LAYOUTS["ragged"]
+        full = slc.Plan(layout, device=-1)
+        rng = np.random.default_rng(5)
+        R = 4
+        recs = [craft_records(full, rng, 0, 30) for _ in range(R)]  # same on every rank (seeded)
+        RW = full.record_bytes // 4
+        lens = shard_chunk_lengths(full)
+
+        def sq_units(rec, c0, c1):
+            t = Fraction(0)
+            for c in range(c0, c1):
+                _, dq = oracle.decode_chunk(rec[c * RW:(c + 1) * RW], lens[c])
+                t += sum(Fraction(float(x)) ** 2 for x in dq)
+            return int(t * (1 << 48))
+
+        p = slc.Plan(layout, rank=rank, nranks=world, device=-1)
+        c0, c1 = p.info.first_chunk, p.info.first_chunk + p.n_chunks
+        mine = [sq_units(r, c0, c1) for r in recs]
+        limbs = torch.tensor([[(v >> (32 * i)) & 0xFFFFFFFF for i in range(4)] for v in mine], dtype=torch.int64)
+        mn = MedianNorm.__new__(MedianNorm)
+        mn.group, mn.world = None, world
+        mn.reduce_limbs(limbs)
+        got = [sum(int(x) << (32 * i) for i, x in enumerate(row)) for row in limbs.tolist()]
+        want = [sq_units(r, 0, full.n_chunks) for r in recs]
+        q.put((rank, got == want))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_median_norm_limb_allreduce_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_median_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

@@ -289,3 +289,89 @@ def test_generator_cuda_twin_bitwise():
     buf = torch.empty(5000, dtype=torch.bfloat16, device=DEV)
     slcgen.fill_cuda(buf, slcgen.WHAT_THETA, 1, 0, 999)
     assert np.array_equal(buf.view(torch.int16).cpu().numpy().view(np.uint16), ref)
+
+
+# ---------------------------------------------------------------- median-norm (R#20)
+def _chunks_of(plan, rec_words):
+    from helpers import shard_chunk_lengths
+    RW = plan.record_bytes // 4
+    lens = shard_chunk_lengths(plan)
+    return [(rec_words[i * RW:(i + 1) * RW], n) for i, n in enumerate(lens)]
+
+
+def _limbs_value(limbs_row):
+    return sum(int(x) << (32 * i) for i, x in enumerate(np.asarray(limbs_row, np.int64).view(np.uint64)))
+
+
+def _exact_sq_units(plan, rec_words):
+    """sum of dq^2 over the payload, as an integer in units of 2^-48 (Fractions, oracle decode)."""
+    from fractions import Fraction
+    tot = Fraction(0)
+    for rec, n in _chunks_of(plan, rec_words):
+        _, dq = oracle.decode_chunk(rec, n)
+        tot += sum(Fraction(float(x)) ** 2 for x in dq)
+    v = tot * (1 << 48)
+    assert v.denominator == 1
+    return int(v)
+
+
+@pytest.mark.parametrize("exps", [(2, 12), (0, 30)])
+def test_median_norm_weights_parity(exps):
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout)
+    rng = np.random.default_rng(300 + exps[1])
+    R = 7
+    ref_recs = [craft_records(plan, rng, *exps) for _ in range(R)]
+    ref_recs[3] = ref_recs[0].copy()
+    ref_recs[3].reshape(-1, plan.record_bytes // 4)[:, -1] = 0  # a zero-norm peer passes through
+    recs = [torch.from_numpy(r.view(np.uint8).copy()).to(DEV) for r in ref_recs]
+    limbs = torch.zeros((R, 4), dtype=torch.int64, device=DEV)
+    plan.payload_sqnorm(recs, limbs)
+    w = torch.zeros(R, dtype=torch.float32, device=DEV)
+    nrm = torch.zeros(R, dtype=torch.float64, device=DEV)
+    plan.median_norm_weights(limbs, w, nrm)
+    assert plan.get_status() == slc.OK
+    L = limbs.cpu().numpy()
+    for r in range(R):
+        assert _limbs_value(L[r]) == _exact_sq_units(plan, ref_recs[r])
+    ref_norms = [oracle.payload_norm(_chunks_of(plan, rr)) for rr in ref_recs]
+    assert np.array_equal(nrm.cpu().numpy(), np.array(ref_norms))
+    ref_w = oracle.median_norm_weights(ref_norms)
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), ref_w.view(np.uint32))
+    assert float(w[3]) == 1.0
+    # the weighted fused update with the device weights == the oracle's weighted Eq. 2
+    ids = [bytes(rng.integers(0, 256, 16, dtype=np.uint8)) for _ in range(R)]
+    hdrs = [slc.make_header(plan, ids[r], base_round=1) for r in range(R)]
+    theta, _, _ = make_device_inputs(plan, layout, 31, 0)
+    thetas = [host_segment(layout, s, slcgen.WHAT_THETA, 31, 0) for s in plan.segments]
+    plan.outer_update(theta, 1.0, records=recs, hdrs=hdrs, weights_dev=w)
+    assert plan.get_status() == slc.OK
+    ref = oracle_update_shard(plan, thetas, ref_recs, 1.0, peer_ids=np.frombuffer(b"".join(ids), np.uint8),
+                              weights=ref_w)
+    for s, t in zip(plan.segments, ref):
+        assert np.array_equal(bits(seg_view(theta, s).cpu().numpy()), bits(t))
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_payload_sqnorm_sharding_invariance(nranks):
+    """Limbs of the shards add up exactly to the single-shard limbs' value."""
+    layout = layouts.LAYOUTS["ragged"]
+    full = slc.Plan(layout)
+    rng = np.random.default_rng(40 + nranks)
+    R = 3
+    ref_recs = [craft_records(full, rng, 0, 30) for _ in range(R)]
+    recs = [torch.from_numpy(r.view(np.uint8).copy()).to(DEV) for r in ref_recs]
+    limbs = torch.zeros((R, 4), dtype=torch.int64, device=DEV)
+    full.payload_sqnorm(recs, limbs)
+    want = [_limbs_value(x) for x in limbs.cpu().numpy()]
+    tot = [0] * R
+    for g in range(nranks):
+        p = slc.Plan(layout, rank=g, nranks=nranks)
+        rb = p.record_bytes
+        lo = p.info.first_chunk * rb
+        part = [r[lo:lo + p.payload_bytes] for r in recs]
+        lg = torch.zeros((R, 4), dtype=torch.int64, device=DEV)
+        if p.n_chunks:
+            p.payload_sqnorm(part, lg)
+        tot = [a + _limbs_value(x) for a, x in zip(tot, lg.cpu().numpy())]
+    assert tot == want
