@@ -233,6 +233,42 @@ struct Pipe {
     const int total = a.R * k_eff;
     cp_async_wait1();
     const bool owner = KC ? (t & 7) == 7 : (t & 31) == (RW - 1) % 32;
+    if (a.weighted && owner) {
+      // weighted: the exact products w_r * S_b (35 significant bits) as M * 2^E,
+      // M < 2^35; hi word = M >> 32 | (E + 1024) << 8 | sign(w) << 30
+      int emin = 0x7FFFFFFF, emax = (int)0x80000000;
+      for (int r = KC ? (t >> 3) : (t >> 5); r < a.R; r += KC ? NT / 8 : NT / 32) {
+        const uint32_t sw = srec[r * SR + RW - 1];
+        const float wf = (float)peer_weight(a, r);
+        uint32_t fw[4];
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          const uint32_t h = (sw >> (16 * b)) & 0xFFFFu;
+          const double d = __dmul_rn((double)wf, (double)__half2float(__ushort_as_half((unsigned short)h)));
+          const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+          const int ed = (int)((db >> 52) & 0x7FF);
+          unsigned long long M = 0;
+          int E = 0;
+          if (!isfinite(d) || ((h >> 10) & 0x1Fu) == 0x1Fu) {
+            emax = 1 << 20;  // non-finite: this chunk takes the sequential path
+          } else if (d != 0.0) {
+            // |d| = (2^52 + frac) * 2^(ed - 1075) for normal d (products are never fp64-subnormal)
+            M = ((db & 0xFFFFFFFFFFFFFull) | (1ull << 52)) >> 18;
+            E = ed - 1075 + 18;
+            if (M & ~((1ull << 35) - 1)) emax = 1 << 20;  // not a 35-bit product: sequential path
+            emin = min(emin, E);
+            emax = max(emax, E);
+          }
+          fw[2 * b] = (uint32_t)M;
+          fw[2 * b + 1] = (uint32_t)(M >> 32) | ((uint32_t)(E + 1024) & 0xFFFu) << 8 | (wf < 0.0f ? 1u << 30 : 0u);
+        }
+        tab[r] = make_int4((int)fw[0], (int)fw[1], (int)fw[2], (int)fw[3]);
+      }
+      if (emin <= emax) {
+        atomicMin(&erange[buf].x, emin);
+        atomicMax(&erange[buf].y, emax);
+      }
+    }
     if (!a.weighted && owner) {
       // this thread copied the scale word of records r (issue_records), so it
       // may read them without a barrier: F = fp16 scale as a multiple of 2^-24
@@ -269,14 +305,29 @@ struct Pipe {
     //        re-zeroed by atomicExch
     //  WIDE  unit weights otherwise: the R#17 hi*2^20 + lo split over two int32
     //        arrays (acc, acc + C)
-    //  W     weights: fp64 in canonical peer order (one warp)
-    int mode;  // 0 FAST, 1 WIDE, 2 W
+    //  WFAST weights, and the chunk's exact products w_r * S_b within a
+    //        2^(17 - ceil(log2 R)) range: every partial sum of the oracle's
+    //        fp64 canonical-order sum is then exact, so the order-free exact
+    //        fixed-point sum (M << (E - Emin), split over two int32 arrays) is
+    //        bitwise the same
+    //  W     weights otherwise: fp64 in canonical peer order (one warp)
+    int mode;  // 0 FAST, 1 WIDE, 2 W, 3 WFAST
     int sh = 0;
+    const int rbits = a.R > 1 ? 32 - __clz(a.R - 1) : 0;  // ceil(log2 R)
+    const int Lw = 31 - rbits;                            // WFAST lo/hi split
     if (a.weighted) {
-      mode = 2;
+      const int2 er = erange[buf];
+      if (er.x > er.y) {
+        mode = 3;  // every product is zero
+        sh = 0;
+      } else if (er.y - er.x + 35 + rbits <= 52) {
+        mode = 3;
+        sh = er.x;
+      } else {
+        mode = 2;
+      }
     } else {
       const int2 er = erange[buf];
-      const int rbits = a.R > 1 ? 32 - __clz(a.R - 1) : 0;  // ceil(log2 R)
       if (er.x > er.y || er.y - er.x + 11 + rbits <= 31) {
         mode = 0;
         sh = er.x > er.y ? 0 : er.x - 1;
@@ -315,7 +366,7 @@ struct Pipe {
         spos[r * kk + 32 * h + lane] = (uint16_t)p;
         atomicAdd(&acc32[p], v);
       }
-    } else if (mode < 2) {
+    } else if (mode != 2) {
       // pass 1: every entry into the exact accumulator; remember its position.
       // Full chunks: warp w takes 32-slot units (record r, slots 32h..32h+31)
       // with lane-constant bit offsets; partial chunks walk entries.
@@ -354,6 +405,14 @@ struct Pipe {
           int v = ok ? (int)__funnelshift_r(flo, fhi, sh) : 0;  // F >> sh, exact
           if (code & 1u) v = -v;
           atomicAdd(&acc32[p], v);
+        } else if (mode == 3) {
+          const unsigned long long M = ((unsigned long long)(fhi & 0xFFu) << 32) | flo;
+          const int E = (int)((fhi >> 8) & 0xFFFu) - 1024;
+          const unsigned long long v = (ok && M) ? M << (E - sh) : 0ull;  // < 2^(52 - rbits)
+          int lo = (int)(v & ((1ull << Lw) - 1)), hi = (int)(v >> Lw);
+          if (((code & 1u) != 0) != (((fhi >> 30) & 1u) != 0)) { lo = -lo; hi = -hi; }
+          atomicAdd(&acc32[p], lo);
+          atomicAdd(&acc32[C + p], hi);
         } else {
           int lo = ok ? (int)(flo & 0xFFFFFu) : 0, hi = ok ? (int)__funnelshift_r(flo, fhi, 20) : 0;
           if (code & 1u) { lo = -lo; hi = -hi; }
@@ -386,7 +445,7 @@ struct Pipe {
       }
     }
     __syncthreads();  // scatter complete
-    if (t == 0) erange[buf] = make_int2(31, 0);  // read by every thread before the barrier above
+    if (t == 0) erange[buf] = make_int2(0x7FFFFFFF, (int)0x80000000);  // read by every thread before the barrier above
 
     // pass 2: Delta only at touched positions; untouched dlt stay +0.  The
     // oracle's Delta = (float)(acc * invR) with acc = V * 2^(sh-24) exactly,
@@ -406,6 +465,15 @@ struct Pipe {
         // exact: hi*2^20 + lo (|.| < 2^53) is representable; duplicates write the same value
         const double sd = __fma_rn((double)acc32[C + p], 0x1p20, (double)acc32[p]);
         dlt[p] = sd == 0.0 ? 0.0f : __double2float_rn(__dmul_rn(sd, c24));
+      }
+    } else if (mode == 3) {
+      // acc = (hi * 2^Lw + lo) * 2^Emin exactly (|.| < 2^52 before the exact scaling)
+      const double ce = __longlong_as_double((long long)(1023 + sh) << 52);
+      const double cl = __longlong_as_double((long long)(1023 + Lw) << 52);
+      for (int s = t; s < total; s += NT) {
+        const int p = spos[s];
+        const double sd = __fma_rn((double)acc32[C + p], cl, (double)acc32[p]);
+        dlt[p] = sd == 0.0 ? 0.0f : __double2float_rn(__dmul_rn(__dmul_rn(sd, ce), invR));
       }
     } else {
       for (int s = t; s < total; s += NT) {
@@ -458,7 +526,7 @@ struct Pipe {
     }
     // WIDE / W: the accumulator is re-zeroed where it was touched (the next
     // scatter follows a barrier); FAST re-zeroed it in pass 2
-    if (mode == 1) {
+    if (mode == 1 || mode == 3) {
       for (int s = t; s < total; s += NT) {
         const int p = spos[s];
         acc32[p] = 0;
@@ -505,7 +573,7 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   for (int i = t; i < C / 4; i += NT) reinterpret_cast<float4*>(P.dlt)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (t < 2) P.srec0[t * P.bufw + a.R * SR] = 0u;  // rec_index may read one word past the last record
 
-  if (t < 2) P.erange[t] = make_int2(31, 0);
+  if (t < 2) P.erange[t] = make_int2(0x7FFFFFFF, (int)0x80000000);
   if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
   __syncthreads();
   float thA[16], thB[16];

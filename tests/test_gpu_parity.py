@@ -128,6 +128,36 @@ def test_aggregate_crafted_records(R, exps, dtype, agg_kernel):
         assert np.array_equal(bits(got.numpy()), bits(t))
 
 
+@pytest.mark.parametrize("R", [2, 20, 40])
+@pytest.mark.parametrize("exps,wspan", [((4, 9), 1.0), ((4, 9), 64.0), ((0, 30), 1.0), ((2, 14), 1e4)])
+def test_weighted_aggregate_crafted(R, exps, wspan, agg_kernel):
+    """Weighted Eq. 2 (median-norm weights enter as w_r) on crafted
+    payloads: narrow scale / weight ranges take the exact fixed-point path
+    (bitwise the oracle's fp64 canonical-order sum, which is exact there),
+    wide ones the sequential fp64 path."""
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout)
+    rng = np.random.default_rng(500 + R + exps[1] + int(wspan))
+    ref_recs = [craft_records(plan, rng, *exps) for _ in range(R)]
+    recs = [torch.from_numpy(r.view(np.uint8).copy()).to(DEV) for r in ref_recs]
+    ids = [bytes(rng.integers(0, 256, 16, dtype=np.uint8)) for _ in range(R)]
+    hdrs = [slc.make_header(plan, ids[r], base_round=2) for r in range(R)]
+    w = np.exp(rng.uniform(-np.log(wspan), np.log(wspan), R)).astype(np.float32) if wspan > 1 else \
+        rng.uniform(0.5, 1.5, R).astype(np.float32)
+    got = torch.zeros(plan.shard_elems, device=DEV)
+    plan.decode_aggregate(recs, got, hdrs=hdrs, weights=w)
+    wd = torch.from_numpy(w).to(DEV)
+    got2 = torch.zeros(plan.shard_elems, device=DEV)
+    plan.decode_aggregate(recs, got2, hdrs=hdrs, weights_dev=wd)
+    assert plan.get_status() == slc.OK
+    thetas = [np.zeros(s.n_elems, np.float32) for s in plan.segments]
+    ref = oracle_update_shard(plan, thetas, ref_recs, 1.0, peer_ids=np.frombuffer(b"".join(ids), np.uint8),
+                              weights=w, only_delta=True)
+    for s, d in zip(plan.segments, ref):
+        assert np.array_equal(bits(seg_view(got, s).cpu().numpy()), bits(d))
+        assert np.array_equal(bits(seg_view(got2, s).cpu().numpy()), bits(d))
+
+
 @pytest.mark.parametrize("R", [3, 20])
 @pytest.mark.parametrize("offset", [4, 8, 12])
 def test_aggregate_misaligned_record_buffers(R, offset, agg_kernel):
