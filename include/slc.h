@@ -42,7 +42,8 @@ typedef enum {
   SLC_ERR_INVALID_DATA = 2,     /* non-finite input or fp16 scale overflow (latched)  */
   SLC_ERR_STALE = 3,            /* peer headers disagree: base_round, layout digest, geometry */
   SLC_ERR_CUDA = 4,             /* a CUDA runtime call failed                         */
-  SLC_ERR_UNSUPPORTED = 5       /* geometry without a compiled kernel                 */
+  SLC_ERR_UNSUPPORTED = 5,      /* geometry without a compiled kernel                 */
+  SLC_ERR_FORMAT = 6            /* wire bytes: bad magic / version, truncated  */
 } slc_status;
 
 typedef enum { SLC_F32 = 0, SLC_BF16 = 1 } slc_dtype; /* dtype of theta / theta_local; e is fp32 */
@@ -204,6 +205,34 @@ slc_status slc_decode_aggregate_wdev(slc_plan* plan, const slc_payload_hdr* hdrs
 slc_status slc_outer_update_wdev(slc_plan* plan, void* theta_dev, const slc_payload_hdr* hdrs_host,
                                  const void* const* records_dev_host, int32_t R, const float* weights_dev,
                                  float alpha, void* stream);
+
+/* NEXT row f2: SPEC's SLC1 wire format (the paper fixes no byte
+ * layout, P:93 fixes 12 bits per index).  A message is the 65-byte header
+ * (magic "SLC1", version 1, base-round u64, peer-id 16 B, layout-digest 32 B,
+ * chunk count u32; big-endian) followed by one encoding per chunk in global
+ * chunk order: count u16 (= k_eff), scale-lo and scale-hi (fp16 bits, u16),
+ * the k_eff indices as index_bits-bit big-endian fields concatenated and
+ * zero-padded to a byte, the k_eff 2-bit symbols (sign*2 + bucket, reading
+ * R#27) packed likewise.  A shard's encodings are one contiguous byte range.
+ *
+ * slc_wire_layout: this shard's encodings take body_bytes bytes starting
+ *   body_offset bytes after the header.
+ * slc_wire_encode: records_dev (this shard's records, slc_compress layout) ->
+ *   wire_dev[body_bytes] (device).  Asynchronous on stream.
+ * slc_wire_decode: wire_dev[body_bytes] -> records_dev, validating every chunk
+ *   (count == k_eff, indices strictly increasing and < the chunk length, zero
+ *   padding, scales finite, >= 0, lo <= hi); a violation latches
+ *   SLC_ERR_INVALID_DATA (reported by slc_get_status) and zeroes that record.
+ * slc_wire_header_write / _read: host-side header (65 bytes).  _read returns
+ *   SLC_ERR_FORMAT on a short buffer, bad magic or version; it fills magic,
+ *   version, base_round, peer_id, layout_digest (geometry and chunk range are
+ *   not on the wire: the caller's plan supplies them). */
+slc_status slc_wire_layout(const slc_plan* plan, int64_t* body_bytes_host, int64_t* body_offset_host);
+slc_status slc_wire_encode(slc_plan* plan, const void* records_dev, void* wire_dev, void* stream);
+slc_status slc_wire_decode(slc_plan* plan, const void* wire_dev, void* records_dev, void* stream);
+slc_status slc_wire_header_write(const slc_payload_hdr* hdr_host, int64_t total_chunks, uint8_t out_host[65]);
+slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payload_hdr* hdr_host,
+                                int64_t* total_chunks_host);
 
 /* Latched device-side status of the plan.  synchronize != 0: wait for the
  * plan's device, read and clear the device error word.  synchronize == 0:

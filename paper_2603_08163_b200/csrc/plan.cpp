@@ -36,6 +36,10 @@ struct slc_plan {
   const void* tmap_ptrs[3] = {nullptr, nullptr, nullptr};
   slc_status latched = SLC_OK;
   uint8_t digest[32];
+  // f2 wire format: per-chunk byte offsets of the shard's encodings, their
+  // total, and the offset of the shard's first encoding in the message body
+  int64_t* d_wire_off = nullptr;
+  int64_t wire_bytes = 0, wire_offset = 0;
 };
 
 namespace {
@@ -344,6 +348,31 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
   }
   p->n_chunks = (int64_t)table.size();
   p->shard_elems = shard_off;
+  // wire encodings: 6 + ceil(k_eff*ib/8) + ceil(2 k_eff/8) bytes per chunk
+  auto wire_size = [&](int64_t len) {
+    const int64_t ke = std::max<int64_t>(1, (int64_t)geom->k * len / geom->chunk);
+    return 6 + (ke * geom->index_bits + 7) / 8 + (2 * ke + 7) / 8;
+  };
+  std::vector<int64_t> wire_off(table.size());
+  for (size_t i = 0; i < table.size(); i++) {
+    wire_off[i] = p->wire_bytes;
+    p->wire_bytes += wire_size(table[i].len);
+  }
+  {
+    int64_t c = 0;  // global chunks before first_chunk, tensor by tensor
+    for (const auto& t : p->layout) {
+      const int64_t nc = tensor_chunks(t, *geom);
+      if (c >= p->first_chunk) break;
+      const int64_t take = std::min(nc, p->first_chunk - c);
+      if (blocked(t, geom->block)) {
+        p->wire_offset += take * wire_size(geom->chunk);
+      } else {
+        const int64_t n = numel(t);
+        for (int64_t q = 0; q < take; q++) p->wire_offset += wire_size(std::min<int64_t>(geom->chunk, n - q * geom->chunk));
+      }
+      c += take;
+    }
+  }
 
   if (device < 0) {  // host-only plan: geometry / partition queries, no compute
     *out = p;
@@ -360,8 +389,12 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     ce = cudaMalloc(&p->d_chunks, table.size() * sizeof(ChunkDesc));
     if (ce == cudaSuccess)
       ce = cudaMemcpy(p->d_chunks, table.data(), table.size() * sizeof(ChunkDesc), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_wire_off, wire_off.size() * sizeof(int64_t));
+    if (ce == cudaSuccess)
+      ce = cudaMemcpy(p->d_wire_off, wire_off.data(), wire_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
   }
   if (ce != cudaSuccess) {
+    if (p->d_wire_off) cudaFree(p->d_wire_off);
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
@@ -522,6 +555,79 @@ slc_status slc_median_norm_weights(slc_plan* p, int32_t R, const uint64_t* sqnor
                      p);
 }
 
+slc_status slc_wire_layout(const slc_plan* p, int64_t* body_bytes, int64_t* body_offset) {
+  if (!p || !body_bytes || !body_offset) return SLC_ERR_INVALID_ARGUMENT;
+  *body_bytes = p->wire_bytes;
+  *body_offset = p->wire_offset;
+  return SLC_OK;
+}
+
+static slc::WireArgs wire_args(slc_plan* p) {
+  slc::WireArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.chunks = p->d_chunks;
+  a.n_chunks = p->n_chunks;
+  a.wire_off = p->d_wire_off;
+  a.err = p->d_err;
+  a.g = p->g;
+  return a;
+}
+
+slc_status slc_wire_encode(slc_plan* p, const void* records, void* wire, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!records || !wire || (((uintptr_t)records) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+  slc::WireArgs a = wire_args(p);
+  a.rec = static_cast<const uint32_t*>(records);
+  a.wire = static_cast<uint8_t*>(wire);
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_wire(a, true, static_cast<cudaStream_t>(stream)), p);
+}
+
+slc_status slc_wire_decode(slc_plan* p, const void* wire, void* records, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!records || !wire || (((uintptr_t)records) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+  slc::WireArgs a = wire_args(p);
+  a.wire_in = static_cast<const uint8_t*>(wire);
+  a.rec_out = static_cast<uint32_t*>(records);
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_wire(a, false, static_cast<cudaStream_t>(stream)), p);
+}
+
+static void put_be(uint8_t* o, uint64_t v, int n) {
+  for (int i = 0; i < n; i++) o[i] = (uint8_t)(v >> (8 * (n - 1 - i)));
+}
+static uint64_t get_be(const uint8_t* o, int n) {
+  uint64_t v = 0;
+  for (int i = 0; i < n; i++) v = (v << 8) | o[i];
+  return v;
+}
+
+slc_status slc_wire_header_write(const slc_payload_hdr* h, int64_t total_chunks, uint8_t out[65]) {
+  if (!h || !out || total_chunks < 0 || total_chunks > 0xFFFFFFFFll) return SLC_ERR_INVALID_ARGUMENT;
+  std::memcpy(out, "SLC1", 4);
+  out[4] = 1;
+  put_be(out + 5, h->base_round, 8);
+  std::memcpy(out + 13, h->peer_id, 16);
+  std::memcpy(out + 29, h->layout_digest, 32);
+  put_be(out + 61, (uint64_t)total_chunks, 4);
+  return SLC_OK;
+}
+
+slc_status slc_wire_header_read(const uint8_t* in, int64_t nbytes, slc_payload_hdr* h, int64_t* total_chunks) {
+  if (!in || !h || !total_chunks) return SLC_ERR_INVALID_ARGUMENT;
+  if (nbytes < 65 || std::memcmp(in, "SLC1", 4) != 0 || in[4] != 1) return SLC_ERR_FORMAT;
+  std::memset(h, 0, sizeof(*h));
+  std::memcpy(h->magic, "SLC1", 4);
+  h->version = 1;
+  h->base_round = get_be(in + 5, 8);
+  std::memcpy(h->peer_id, in + 13, 16);
+  std::memcpy(h->layout_digest, in + 29, 32);
+  *total_chunks = (int64_t)get_be(in + 61, 4);
+  return SLC_OK;
+}
+
 slc_status slc_get_status(slc_plan* p, int32_t synchronize) {
   if (!p) return SLC_ERR_INVALID_ARGUMENT;
   slc_status st = p->latched;
@@ -545,6 +651,7 @@ void slc_plan_destroy(slc_plan* p) {
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
+    if (p->d_wire_off) cudaFree(p->d_wire_off);
   }
   delete p;
 }
@@ -557,6 +664,7 @@ const char* slc_status_string(slc_status s) {
     case SLC_ERR_STALE: return "stale submission (base round / layout digest / geometry mismatch)";
     case SLC_ERR_CUDA: return "CUDA runtime error";
     case SLC_ERR_UNSUPPORTED: return "unsupported geometry";
+    case SLC_ERR_FORMAT: return "format error";
   }
   return "unknown status";
 }

@@ -89,6 +89,20 @@ struct AggArgs {
   Geom g;
 };
 
+// f2 wire format (wire.cu)
+struct WireArgs {
+  const ChunkDesc* chunks;
+  int64_t n_chunks;
+  const int64_t* wire_off;  // per chunk: byte offset of its encoding from the shard's first chunk
+  const uint32_t* rec;      // encode: records in
+  uint8_t* wire;            // encode: bytes out
+  const uint8_t* wire_in;   // decode: bytes in
+  uint32_t* rec_out;        // decode: records out
+  uint32_t* err;
+  Geom g;
+};
+cudaError_t launch_wire(const WireArgs& a, bool encode, cudaStream_t s);
+
 // launchers (return cudaGetLastError())
 cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one CTA per chunk, any compiled C (reference kernel for the pipelined one)

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence, Tuple
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SLC_LIB") or os.path.join(_HERE, "libslc.so")  # SLC_LIB: tuning variants
 
-OK, INVALID_ARGUMENT, INVALID_DATA, STALE, CUDA_ERROR, UNSUPPORTED = range(6)
+OK, INVALID_ARGUMENT, INVALID_DATA, STALE, CUDA_ERROR, UNSUPPORTED, FORMAT_ERROR = range(7)
 F32, BF16 = 0, 1
 MAX_PEERS = 256
 
@@ -77,6 +77,11 @@ def _load():
         "slc_median_norm_weights": (ctypes.c_int, [P, ctypes.c_int32, P, P, P, P]),
         "slc_decode_aggregate_wdev": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
         "slc_outer_update_wdev": (ctypes.c_int, [P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
+        "slc_wire_layout": (ctypes.c_int, [P, pp(ctypes.c_int64), pp(ctypes.c_int64)]),
+        "slc_wire_encode": (ctypes.c_int, [P, P, P, P]),
+        "slc_wire_decode": (ctypes.c_int, [P, P, P, P]),
+        "slc_wire_header_write": (ctypes.c_int, [pp(PayloadHdr), ctypes.c_int64, P]),
+        "slc_wire_header_read": (ctypes.c_int, [P, ctypes.c_int64, pp(PayloadHdr), pp(ctypes.c_int64)]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
         "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -92,7 +97,8 @@ _lib = _load()
 
 EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_record_bytes", "slc_layout_digest",
             "slc_compress", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
-            "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_get_status",
+            "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
+            "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
             "slc_plan_destroy", "slc_status_string"]
 
 
@@ -157,6 +163,21 @@ class SegmentInfo:
     cols: int
     first_chunk: int
     n_chunks: int
+
+
+def wire_header_write(hdr: PayloadHdr, total_chunks: int) -> bytes:
+    out = (ctypes.c_uint8 * 65)()
+    _check(_lib.slc_wire_header_write(ctypes.byref(hdr), total_chunks, out), "slc_wire_header_write")
+    return bytes(out)
+
+
+def wire_header_read(buf: bytes):
+    """(header, total_chunks); SlcError(FORMAT_ERROR) on a bad header."""
+    h = PayloadHdr()
+    n = ctypes.c_int64()
+    b = (ctypes.c_uint8 * max(1, len(buf))).from_buffer_copy(bytes(buf) or b"\0")
+    _check(_lib.slc_wire_header_read(b, len(buf), ctypes.byref(h), ctypes.byref(n)), "slc_wire_header_read")
+    return h, n.value
 
 
 def make_header(plan: "Plan", peer_id: bytes, base_round: int = 0) -> PayloadHdr:
@@ -251,6 +272,19 @@ class Plan:
             return
         _check(_lib.slc_decode_aggregate(self._h, h, ptrs, R, w, _dptr(agg), _stream_ptr(stream)),
                "slc_decode_aggregate")
+
+    # ---- SLC1 wire format (NEXT row f2)
+    def wire_layout(self):
+        """(body_bytes, body_offset) of this shard's chunk encodings in the message body."""
+        b, o = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.slc_wire_layout(self._h, ctypes.byref(b), ctypes.byref(o)), "slc_wire_layout")
+        return b.value, o.value
+
+    def wire_encode(self, records, wire, stream=None) -> None:
+        _check(_lib.slc_wire_encode(self._h, _dptr(records), _dptr(wire), _stream_ptr(stream)), "slc_wire_encode")
+
+    def wire_decode(self, wire, records, stream=None) -> None:
+        _check(_lib.slc_wire_decode(self._h, _dptr(wire), _dptr(records), _stream_ptr(stream)), "slc_wire_decode")
 
     # ---- median-norm normalisation (P:101, DESIGN.md R#20)
     def payload_sqnorm(self, records: Sequence, out, hdrs=None, stream=None) -> None:

@@ -405,3 +405,70 @@ def test_payload_sqnorm_sharding_invariance(nranks):
             p.payload_sqnorm(part, lg)
         tot = [a + _limbs_value(x) for a, x in zip(tot, lg.cpu().numpy())]
     assert tot == want
+
+
+# ---------------------------------------------------------------- SLC1 wire format (NEXT row f2)
+@pytest.mark.parametrize("name,nranks", [("ragged", 1), ("ragged", 3), ("1m-1d", 2)])
+def test_wire_encode_decode_parity(name, nranks):
+    """GPU encode of compress output == the oracle's bit-string encoding of the
+    same records (byte for byte, S:143); decode(encode(x)) == x bit for bit;
+    the shards' bodies concatenate to the whole message body."""
+    from oracle import wire
+    from helpers import shard_chunk_lengths
+    layout = layouts.LAYOUTS[name]
+    g = oracle.geom()
+    bodies = []
+    for rank in range(nranks):
+        plan = slc.Plan(layout, rank=rank, nranks=nranks)
+        if plan.n_chunks == 0:
+            continue
+        theta, tl, ef, rec = _compress_gpu(plan, layout, 17, 1, "f32", 4, True)
+        body_bytes, body_off = plan.wire_layout()
+        w = torch.zeros(body_bytes, dtype=torch.uint8, device=DEV)
+        plan.wire_encode(rec, w)
+        rw = rec.cpu().numpy().view(np.uint32).reshape(-1, plan.record_bytes // 4)
+        lens = shard_chunk_lengths(plan)
+        want = b"".join(wire.encode_chunk(*wire.record_to_chunk(r, oracle.effective_k(n, g))) for r, n in zip(rw, lens))
+        got = bytes(w.cpu().numpy())
+        assert got == want
+        back = torch.zeros_like(rec)
+        plan.wire_decode(w, back)
+        assert plan.get_status() == slc.OK
+        assert torch.equal(back, rec)
+        bodies.append((body_off, got))
+    off = 0
+    for o, b in bodies:
+        assert o == off
+        off += len(b)
+
+
+def test_wire_decode_rejects_invalid_chunks():
+    from oracle import wire
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout)
+    theta, tl, ef, rec = _compress_gpu(plan, layout, 19, 2, "f32", 0, True)
+    nb, _ = plan.wire_layout()
+    w = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    plan.wire_encode(rec, w)
+    good = w.cpu().numpy().copy()
+    size0 = wire.chunk_wire_bytes(64)
+    cases = {
+        "count": lambda b: b.__setitem__(1, b[1] ^ 1),
+        "scale_inf": lambda b: b.__setitem__(4, 0x7C),
+        "lo_gt_hi": lambda b: (b.__setitem__(2, 0x7B), b.__setitem__(3, 0xFF)),
+        "order": lambda b: b.__setitem__(6, 0xFF),  # first index -> >= 0xFF0 > the second
+        "padding": None,
+    }
+    for name, f in cases.items():
+        b = good.copy()
+        if f is None:
+            continue  # 64 indices x 12 bits and 64 codes x 2 bits fill whole bytes: no padding at k = 64
+        f(b)
+        back = torch.zeros_like(rec)
+        plan.wire_decode(torch.from_numpy(b).to(DEV), back)
+        assert plan.get_status() == slc.INVALID_DATA, name
+    # untouched bytes decode cleanly again (the latch was cleared by get_status)
+    back = torch.zeros_like(rec)
+    plan.wire_decode(torch.from_numpy(good).to(DEV), back)
+    assert plan.get_status() == slc.OK and torch.equal(back, rec)
+    assert size0 == 118
