@@ -84,6 +84,12 @@ struct PipeSmem {
   __host__ __device__ static size_t bytes(int R, int k, int RW) { return off_erange(R, k, RW) + 16; }
 };
 
+#ifndef SLC_AGG_UNROLL
+#define SLC_AGG_UNROLL 1  // unroll of the per-entry loops (independent iterations in flight)
+#endif
+#define SLC_PRAGMA(x) _Pragma(#x)
+#define SLC_UNROLL(n) SLC_PRAGMA(unroll n)
+
 #ifndef SLC_AGG_MINB
 #define SLC_AGG_MINB 3  // CTAs per SM the register budget is sized for (C = 4096)
 #endif
@@ -345,6 +351,7 @@ struct Pipe {
       const int cw = IW + (lane >> 4), csh = 2 * (lane & 15);
       const uint32_t imask = (1u << ib) - 1u;
       const bool check_p = (1 << ib) > len;
+      SLC_UNROLL(SLC_AGG_UNROLL)
       for (int u = t >> 5; u < a.R * KW; u += NT / 32) {
         const int r = u / KW;
         const int h = u - r * KW;
@@ -453,6 +460,7 @@ struct Pipe {
     const double invR = a.invR;
     if (mode == 0) {
       const double cs = __dmul_rn(invR, __longlong_as_double((long long)(1023 + sh - 24) << 52));  // exact
+      SLC_UNROLL(SLC_AGG_UNROLL)
       for (int s = t; s < total; s += NT) {
         const int p = spos[s];
         const int v = atomicExch(&acc32[p], 0);  // exactly one entry of p sees the sum
