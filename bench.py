@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run shard --shard-rank of an N-way FSDP sharding (one GPU's share of a larger job)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--block", type=int, default=64, help="chunk side B (C = B*B; P:88 uses 64)")
+    ap.add_argument("--k", type=int, default=64, help="values per full chunk (P:176: 64)")
     ap.add_argument("--median-norm", action="store_true",
                     help="median-norm weights (P:101): exact payload norms + all-reduce + weighted fused update")
     return ap.parse_args()
@@ -207,9 +209,11 @@ def run_slc(args):
     layout = slcgen.layouts.LAYOUTS[lname]
     if args.shard_of:
         assert world == 1, "--shard-of simulates one rank of a larger job on one GPU"
-        plan = slc.Plan(layout, rank=args.shard_rank, nranks=args.shard_of, dtype=dtype, device=local)
+        plan = slc.Plan(layout, geom=slc.geometry(args.block, args.k), rank=args.shard_rank,
+                        nranks=args.shard_of, dtype=dtype, device=local)
     else:
-        plan = slc.Plan(layout, rank=rank, nranks=world, dtype=dtype, device=local)
+        plan = slc.Plan(layout, geom=slc.geometry(args.block, args.k), rank=rank, nranks=world, dtype=dtype,
+                        device=local)
     gather = sdist.PayloadGather(plan) if world > 1 else None
     shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=True,
                        records=gather.alloc_records() if gather else None)
@@ -311,14 +315,16 @@ def run_slc(args):
         "vs_baseline": None,
         "dtype": "f32" if dtype == "f32" else "bf16-params/f32-ef",
         "data": "synthetic (slcgen: seeded Llama-shaped param sets; random-init values)",
-        "config": {"workload": f"{wl} ({P_total} params), R={R} peers, C=4096 k=64 2-bit, beta={BETA} alpha={ALPHA}",
+        "config": {"workload": f"{wl} ({P_total} params), R={R} peers, C={args.block ** 2} k={args.k} 2-bit, "
+                               f"beta={BETA} alpha={ALPHA}",
                    "params": P_total, "peers": R, "parallelism": f"fsdp-shard{world}",
                    "l2": "inputs > L2 (126 MB): no flush needed"},
         "hbm_gbs": step_gbs_rank * world,
         "hbm_frac_of_peak": step_gbs_rank / peak,
         "roofline": {"bound": "hbm", "kernel": "slc_compress", "achieved": comp_gbs, "peak": peak,
                      "unit": "GB/s", "frac": comp_gbs / peak,
-                     "traffic": ncu_traffic("compress", wl) if R == WORKLOADS[wl][1] else None,
+                     "traffic": (ncu_traffic("compress", wl) if R == WORKLOADS[wl][1] and args.block == 64
+                                 and args.k == 64 and not args.shard_of else None),
                      "algorithmic_bytes_per_launch": comp_bytes, "peak_source": peak_src},
         "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
                     "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
