@@ -38,6 +38,9 @@ using namespace wsel;
 #ifndef SLC_WS_D
 #define SLC_WS_D 3
 #endif
+#ifndef SLC_WS_CAPG
+#define SLC_WS_CAPG 256  // candidate capacity of the any-geometry instantiation (k != 64)
+#endif
 #ifndef SLC_WS_XS
 #define SLC_WS_XS 0  // hand-off slots beyond one per warp
 #endif
@@ -330,7 +333,7 @@ template <int C, bool BF16>
 cudaError_t launch_ws_c(const CompressArgs& a, cudaStream_t s) {
   if (C == 4096 && a.g.k == 64 && a.g.ib == 12)  // the paper's geometry
     return launch_ws_t<C, BF16, 64, 12, 128, 64>(a, s);
-  return launch_ws_t<C, BF16, 0, 0, 256, kMaxK>(a, s);
+  return launch_ws_t<C, BF16, 0, 0, SLC_WS_CAPG, kMaxK>(a, s);
 }
 
 }  // namespace

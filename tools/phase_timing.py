@@ -14,7 +14,8 @@ from slcgen import layouts  # noqa: E402
 
 lib = ctypes.CDLL(slc.LIB_PATH)
 layout = layouts.LAYOUTS[sys.argv[1] if len(sys.argv) > 1 else "llama3.2-1b"]
-plan = slc.Plan(layout)
+plan = slc.Plan(layout, geom=slc.geometry(int(os.environ.get("BLOCK", 64)), int(os.environ.get("K", 64))),
+                rank=0, nranks=int(os.environ.get("NRANKS", 1)))
 th, tl, ef = make_device_inputs(plan, layout, 1, 0, warm_ef=True)
 rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device="cuda")
 buf = (ctypes.c_ulonglong * 8)()
