@@ -94,10 +94,16 @@ struct PipeSmem {
 #define SLC_AGG_MINB 3  // CTAs per SM the register budget is sized for (C = 4096)
 #endif
 
+#ifndef SLC_AGG_GPT
+#define SLC_AGG_GPT 4  // 4-position groups per thread (C/(4*GPT) threads per CTA)
+#endif
+
 template <int C>
 struct PipeCfg {
-  static constexpr int NT = C / 16;
-  static constexpr int MIN_BLOCKS = (C == 4096) ? SLC_AGG_MINB : 4 * SLC_AGG_MINB;
+  static constexpr int GPT = SLC_AGG_GPT;
+  static constexpr int NT = C / (4 * GPT);
+  static constexpr int MIN_BLOCKS = GPT == 4 ? ((C == 4096) ? SLC_AGG_MINB : 4 * SLC_AGG_MINB)
+                                            : ((C == 4096) ? 4 : 16);
   static constexpr int RPQ = ChunkCfg<C>::RPQ;  // 4-element groups per block row
   static constexpr int RPQ_SHIFT = (RPQ == 8) ? 3 : (RPQ == 16 ? 4 : 5);
 };
@@ -135,16 +141,16 @@ __device__ __forceinline__ int64_t generic_offset(const Desc& d, int q, int rpq_
 }
 
 template <int C, bool BF16>
-__device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int t, float th[16]) {
+__device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int t, float th[4 * SLC_AGG_GPT]) {
   using K = PipeCfg<C>;
   if (d.len == C) {
     int64_t o, step;
     full_addr<C>(d, t, o, step);
 #pragma unroll
-    for (int v = 0; v < 4; v++) load_param4<BF16>(theta, o + v * step, 4, &th[4 * v]);
+    for (int v = 0; v < K::GPT; v++) load_param4<BF16>(theta, o + v * step, 4, &th[4 * v]);
   } else {
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
+    for (int v = 0; v < K::GPT; v++) {
       const int q = v * K::NT + t;
       load_param4<BF16>(theta, generic_offset(d, q, K::RPQ_SHIFT), valid_in_group(4 * q, d.len), &th[4 * v]);
     }
@@ -214,7 +220,7 @@ struct Pipe {
   bool bad;
 
   // one chunk: `cur` holds chunk c's theta, `nxt` receives chunk c+G's
-  __device__ __forceinline__ bool step(float (&cur)[16], float (&nxt)[16]) {
+  __device__ __forceinline__ bool step(float (&cur)[4 * K::GPT], float (&nxt)[4 * K::GPT]) {
     const int RWc = KC ? (KC * 12 + 31) / 32 + (2 * KC + 31) / 32 + 1 : a.g.rec_words;
     const int64_t cn = c + G;
     const bool has_next = cn < n;
@@ -497,7 +503,7 @@ struct Pipe {
       int64_t o, stp;
       full_addr<C>(d0, t, o, stp);
 #pragma unroll
-      for (int v = 0; v < 4; v++) {
+      for (int v = 0; v < K::GPT; v++) {
         float4* d4 = reinterpret_cast<float4*>(dlt) + v * NT + t;
         const float4 dv = *d4;
         *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -513,7 +519,7 @@ struct Pipe {
       }
     } else {
 #pragma unroll
-      for (int v = 0; v < 4; v++) {
+      for (int v = 0; v < K::GPT; v++) {
         const int q = v * NT + t;
         float4* d4 = reinterpret_cast<float4*>(dlt) + q;
         const float4 dv = *d4;
@@ -584,7 +590,7 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   if (t < 2) P.erange[t] = make_int2(0x7FFFFFFF, (int)0x80000000);
   if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
   __syncthreads();
-  float thA[16], thB[16];
+  float thA[4 * PipeCfg<C>::GPT], thB[4 * PipeCfg<C>::GPT];
   if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(P.ring[0]), t, thA);
   issue_records<NT, KC>(a, P.c, P.srec0, t, a.g.rec_words);
   cp_async_commit();
