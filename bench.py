@@ -27,7 +27,8 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     "llama3.2-1b": ("llama3.2-1b", 8, "f32"),      # BASELINE configs[1]
     "llama3-8b": ("llama3-8b", 20, "f32"),         # BASELINE configs[2]
-    "covenant-72b": ("covenant-72b", 20, "f32"),   # BASELINE configs[3]
+    "covenant-72b": ("covenant-72b", 20, "f32"),   # BASELINE configs[3] (reading A, R#22)
+    "covenant-72b-b": ("covenant-72b-b", 20, "f32"),  # reading B: untied, every matrix 64x64-blocked
     "llama2-7b": ("llama2-7b", 20, "f32"),         # BASELINE configs[4] base point
     "1m": ("1m-2d", 1, "f32"),                     # BASELINE configs[0]
     "flat-1b": ("flat-1b", 8, "f32"),              # bandwidth probe (contiguous chunks)
