@@ -94,6 +94,9 @@ struct PipeSmem {
 #define SLC_AGG_MINB 3  // CTAs per SM the register budget is sized for (C = 4096)
 #endif
 
+#ifndef SLC_AGG_THETA_NOW
+#define SLC_AGG_THETA_NOW 0  // 1: theta loaded at the start of its own step (single register buffer)
+#endif
 #ifndef SLC_AGG_GPT
 #define SLC_AGG_GPT 4  // 4-position groups per thread (C/(4*GPT) threads per CTA)
 #endif
@@ -226,10 +229,17 @@ struct Pipe {
     const bool has_next = cn < n;
     // descriptors travel through shared memory by cp.async, three chunks ahead:
     // a register load would be consumed (uniform-register move) at once
+#if SLC_AGG_THETA_NOW
+    // theta of THIS chunk, loaded at the start of its step: its HBM latency hides
+    // behind the chunk's own decode (passes 1-2), one register buffer suffices
+    if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(ring[it & 3]), t, cur);
+    if (has_next) issue_records<NT, KC>(a, cn, srec0 + (buf ^ 1) * bufw, t, RWc);
+#else
     if (has_next) {
       if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(ring[(it + 1) & 3]), t, nxt);
       issue_records<NT, KC>(a, cn, srec0 + (buf ^ 1) * bufw, t, RWc);
     }
+#endif
     if (t == 0 && cn + 2 * G < n) cp_async16(&ring[(it + 3) & 3], a.chunks + cn + 2 * G);
     cp_async_commit();
     const Desc d0 = unpack_desc(ring[it & 3]);
@@ -590,15 +600,25 @@ __global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pi
   if (t < 2) P.erange[t] = make_int2(0x7FFFFFFF, (int)0x80000000);
   if (t < 3 && P.c + t * P.G < P.n) P.ring[t] = __ldg(reinterpret_cast<const int4*>(a.chunks + P.c + t * P.G));
   __syncthreads();
-  float thA[4 * PipeCfg<C>::GPT], thB[4 * PipeCfg<C>::GPT];
+  float thA[4 * PipeCfg<C>::GPT];
+#if !SLC_AGG_THETA_NOW
+  float thB[4 * PipeCfg<C>::GPT];
+#endif
+#if !SLC_AGG_THETA_NOW
   if (MODE == kFused) load_theta<C, BF16>(a.theta, unpack_desc(P.ring[0]), t, thA);
+#endif
   issue_records<NT, KC>(a, P.c, P.srec0, t, a.g.rec_words);
   cp_async_commit();
 
+#if SLC_AGG_THETA_NOW
+  for (;;)
+    if (!P.step(thA, thA)) break;
+#else
   for (;;) {
     if (!P.step(thA, thB)) break;
     if (!P.step(thB, thA)) break;
   }
+#endif
   if (P.bad) atomicOr(a.err, kErrNonFinite);
 }
 
