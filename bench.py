@@ -37,6 +37,7 @@ WORKLOADS = {
 
 BETA = 0.95
 ALPHA = 1.0
+SPECIAL_PERIOD = 0  # set from --special-period
 
 
 def parse():
@@ -54,6 +55,8 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run shard --shard-rank of an N-way FSDP sharding (one GPU's share of a larger job)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--special-period", type=int, default=0,
+                    help="1/P of the 4096-element runs degenerate (zero, constant, ties, ...; slcgen)")
     ap.add_argument("--block", type=int, default=64, help="chunk side B (C = B*B; P:88 uses 64)")
     ap.add_argument("--k", type=int, default=64, help="values per full chunk (P:176: 64)")
     ap.add_argument("--median-norm", action="store_true",
@@ -164,7 +167,8 @@ class ShardState:
         offs = np.cumsum([0] + [int(np.prod(s)) for _, s in self.layout])
         for s in self.plan.segments:
             slcgen.fill_cuda(buf[s.shard_offset:s.shard_offset + s.n_elems], what, self.seed, peer,
-                             int(offs[s.tensor]) + s.tensor_begin, warm_ef=self.warm)
+                             int(offs[s.tensor]) + s.tensor_begin, warm_ef=self.warm,
+                             special_period=SPECIAL_PERIOD)
 
     def reset(self, peer=None):
         import slcgen
@@ -197,6 +201,8 @@ def run_slc(args):
     from paper_2603_08163_b200 import slc
     from paper_2603_08163_b200 import dist as sdist
 
+    global SPECIAL_PERIOD
+    SPECIAL_PERIOD = args.special_period
     rank, world, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
@@ -332,6 +338,8 @@ def run_slc(args):
         "gpu_launches": (4 if args.median_norm else 2) * args.steps,
         "clocks": clk.summary(),
     }
+    if args.special_period:
+        out["config"]["special_period"] = args.special_period
     if args.median_norm:
         out["config"]["median_norm"] = ("P:101: exact payload norms (slc_payload_sqnorm) + int64 all-reduce + "
                                         "lower-median weights on device + weighted fused update; in the timed step")
