@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--k", type=int, default=64, help="values per full chunk (P:176: 64)")
     ap.add_argument("--median-norm", action="store_true",
                     help="median-norm weights (P:101): exact payload norms + all-reduce + weighted fused update")
+    ap.add_argument("--ef-offload", action="store_true",
+                    help="row f3 (P:118-132): EF in pinned host memory, swapped in for compress and out "
+                         "(overlapping the fused update) every step")
     return ap.parse_args()
 
 
@@ -232,15 +235,23 @@ def run_slc(args):
             if args.median_norm else None)
 
     stream = torch.cuda.current_stream()
+    offload = None
+    if args.ef_offload:
+        from paper_2603_08163_b200.offload import EFOffload
+        offload = EFOffload(plan, device=dev)
+        offload.host.copy_(shard.ef.cpu())
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
     def step(i=None):
+        ef = offload.swap_in(stream) if offload is not None else shard.ef
         if i is not None:
             ev[i][0].record(stream)
-        plan.compress(shard.theta, shard.theta_local, shard.ef, shard.records, beta=BETA, stream=stream)
+        plan.compress(shard.theta, shard.theta_local, ef, shard.records, beta=BETA, stream=stream)
         if i is not None:
             ev[i][1].record(stream)
+        if offload is not None:
+            offload.swap_out(stream)
         if gather is not None:
             gather.start(shard.records)
         if mnorm is not None:
@@ -250,6 +261,8 @@ def run_slc(args):
             plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
         if gather is not None:
             gather.wait()
+        if offload is not None:
+            offload.wait(stream)
         if i is not None:
             ev[i][2].record(stream)
 
@@ -338,6 +351,8 @@ def run_slc(args):
         "gpu_launches": (4 if args.median_norm else 2) * args.steps,
         "clocks": clk.summary(),
     }
+    if offload is not None:
+        out["config"]["ef_offload"] = time_offload(offload, stream, reps=3)
     if args.special_period:
         out["config"]["special_period"] = args.special_period
     if args.median_norm:
@@ -355,6 +370,30 @@ def run_slc(args):
     if world > 1:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def time_offload(offload, stream, reps=3):
+    """Row f3: the two EF swaps timed alone on the copy stream (host-link bound, 4 B/param each way)."""
+    import torch
+    cs = offload.copy_stream
+    res = {}
+    for name, fn in (("swap_in", lambda: offload.swap_in(stream)), ("swap_out", lambda: offload.swap_out(stream))):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cs)
+            fn()
+            b.record(cs)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = sorted(ts)[len(ts) // 2]
+        res[name + "_ms"] = ms
+        res[name + "_gbs"] = offload.bytes_per_swap / (ms * 1e-3) / 1e9
+    res["bytes_each_way"] = offload.bytes_per_swap
+    res["note"] = ("P:118-132: EF lives in pinned host memory between steps; timed step = swap-in + compress + "
+                   "max(swap-out, fused update); the swaps are host-link bound")
+    return res
 
 
 def time_collectives(plan, gather, shard, R, stream, dev, reps=5):

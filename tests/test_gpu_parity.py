@@ -472,3 +472,39 @@ def test_wire_decode_rejects_invalid_chunks():
     plan.wire_decode(torch.from_numpy(good).to(DEV), back)
     assert plan.get_status() == slc.OK and torch.equal(back, rec)
     assert size0 == 118
+
+
+@pytest.mark.parametrize("release", [False, True])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_ef_offload_parity(release, dtype):
+    """Row f3: EF kept in pinned host memory, swapped in for slc_compress and out after it
+    (overlapping the fused update on the compute stream).  Records and the host EF after the swap-out are
+    bit-identical to the oracle; a second step from the swapped-out EF equals the oracle's second step."""
+    from paper_2603_08163_b200.offload import EFOffload
+    layout = layouts.LAYOUTS["ragged"]
+    plan = slc.Plan(layout, dtype=dtype)
+    theta, tl, ef = make_device_inputs(plan, layout, 5, 2, dtype, 0, True)
+    off = EFOffload(plan, release=release)
+    off.host.copy_(ef.cpu())
+    rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
+    stream = torch.cuda.current_stream()
+    off.compress(theta, tl, rec, beta=0.95, stream=stream)
+    plan.outer_update(theta, 1.0, records=[rec], stream=stream)  # overlaps the swap-out
+    off.wait(stream)
+    torch.cuda.synchronize()
+    assert plan.get_status() == slc.OK
+    ref_rec, ref_ef, _ = oracle_compress_shard(plan, layout, 5, 2, dtype, 0, True)
+    assert np.array_equal(rec.cpu().numpy().view(np.uint32), ref_rec)
+    host = off.host.clone()
+    for s, e in zip(plan.segments, ref_ef):
+        assert np.array_equal(bits(seg_view(host, s).numpy()), bits(e)), f"EF differs in segment {s.tensor}"
+    # second step: resident EF path on copies of the same state must agree bitwise with the offloaded one
+    ef2 = host.to(DEV)
+    th2, tl2 = theta.clone(), tl.clone()
+    rec2 = torch.zeros_like(rec)
+    plan.compress(th2, tl2, ef2, rec2)
+    off.compress(theta, tl, rec, beta=0.95, stream=stream)
+    off.wait(stream)
+    torch.cuda.synchronize()
+    assert torch.equal(rec, rec2)
+    assert torch.equal(off.host, ef2.cpu())
