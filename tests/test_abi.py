@@ -92,3 +92,16 @@ def test_digest(slc):
     assert a == slc.layout_digest(g, [("x", (64, 64))]) and len(a) == 32
     assert a != slc.layout_digest(g, [("w", (64, 128))])
     assert a != slc.layout_digest(slc.geometry(64, 32), [("w", (64, 64))])
+
+
+def test_ef_offload_needs_cuda():
+    """Row f3's swap targets GPU memory: without a device it fails loudly (no host-side fallback)."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    from paper_2603_08163_b200 import slc
+    from paper_2603_08163_b200.offload import EFOffload
+    from slcgen import layouts
+    plan = slc.Plan(layouts.LAYOUTS["ragged"], device=-1)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        EFOffload(plan)
