@@ -147,6 +147,19 @@ slc_status slc_layout_digest(const slc_geometry* geom_host, const slc_tensor* la
 slc_status slc_compress(slc_plan* plan, const void* theta_dev, const void* theta_local_dev, float* ef_dev,
                         float beta, void* records_dev, void* stream);
 
+/* slc_compress restricted to the shard-local chunks [chunk_begin, chunk_begin + n_chunks)
+ * (same buffers and meaning as slc_compress: full-shard theta / theta_local / ef
+ * base pointers, records_dev the full shard record buffer, chunk c at byte
+ * c*record_bytes).  Only those chunks' elements and records are read or
+ * written, so the EF of the other chunks may be absent from device memory —
+ * the piecewise swap of NEXT row f3 (EF swapped in for compression
+ * and out again, overlapped).  Results are bitwise those of slc_compress for
+ * those chunks (chunks are independent).  INVALID_ARGUMENT for a range
+ * outside [0, n_chunks]; n_chunks == 0 is a no-op. */
+slc_status slc_compress_range(slc_plan* plan, int64_t chunk_begin, int64_t n_chunks, const void* theta_dev,
+                              const void* theta_local_dev, float* ef_dev, float beta, void* records_dev,
+                              void* stream);
+
 /* Eq. 2 line 1: agg_dev[shard_elems] (fp32, padding untouched) <-
  * (1/R) sum_r w_r * decode(records_dev_host[r]) over the shard's chunks.
  *   hdrs_host          R headers or NULL (then no checks, given order is canonical)

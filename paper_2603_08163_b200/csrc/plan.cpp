@@ -429,8 +429,15 @@ slc_status slc_plan_segment(const slc_plan* p, int32_t i, slc_segment* o) {
 
 slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local, float* ef, float beta,
                         void* records, void* stream) {
+  if (!p) return SLC_ERR_INVALID_ARGUMENT;
+  return slc_compress_range(p, 0, p->n_chunks, theta, theta_local, ef, beta, records, stream);
+}
+
+slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* theta, const void* theta_local,
+                              float* ef, float beta, void* records, void* stream) {
   if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
-  if (p->n_chunks == 0) return SLC_OK;
+  if (c0 < 0 || nc < 0 || c0 > p->n_chunks || nc > p->n_chunks - c0) return SLC_ERR_INVALID_ARGUMENT;
+  if (nc == 0) return SLC_OK;
   if (!theta || !theta_local || !ef || !records) return SLC_ERR_INVALID_ARGUMENT;
   if (!aligned16(theta) || !aligned16(theta_local) || !aligned16(ef) || (((uintptr_t)records) & 3u))
     return SLC_ERR_INVALID_ARGUMENT;
@@ -438,12 +445,12 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   a.n_elems = p->shard_elems;
   a.n_tmaps = (int32_t)p->h_tmaps.size();
   a.tmaps = p->d_tmaps;
-  a.chunks = p->d_chunks;
-  a.n_chunks = p->n_chunks;
+  a.chunks = p->d_chunks + c0;
+  a.n_chunks = nc;
   a.theta = theta;
   a.theta_local = theta_local;
   a.ef = ef;
-  a.records = static_cast<uint32_t*>(records);
+  a.records = static_cast<uint32_t*>(records) + c0 * p->g.rec_words;
   a.err = p->d_err;
   a.beta = beta;
   a.max_ld = p->max_ld;

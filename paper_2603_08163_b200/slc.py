@@ -71,6 +71,7 @@ def _load():
         "slc_record_bytes": (ctypes.c_int64, [pp(Geometry)]),
         "slc_layout_digest": (ctypes.c_int, [pp(Geometry), pp(Tensor), ctypes.c_int32, P]),
         "slc_compress": (ctypes.c_int, [P, P, P, P, ctypes.c_float, P, P]),
+        "slc_compress_range": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int64, P, P, P, ctypes.c_float, P, P]),
         "slc_decode_aggregate": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
         "slc_outer_update": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
         "slc_payload_sqnorm": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P]),
@@ -96,7 +97,7 @@ def _load():
 _lib = _load()
 
 EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_record_bytes", "slc_layout_digest",
-            "slc_compress", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
+            "slc_compress", "slc_compress_range", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
             "slc_plan_destroy", "slc_status_string"]
@@ -247,6 +248,16 @@ class Plan:
         assert records.numel() * records.element_size() >= self.payload_bytes
         _check(_lib.slc_compress(self._h, _dptr(theta), _dptr(theta_local), _dptr(ef), ctypes.c_float(beta),
                                  _dptr(records), _stream_ptr(stream)), "slc_compress")
+
+    def compress_range(self, chunk_begin: int, n_chunks: int, theta, theta_local, ef, records, beta: float = 0.95,
+                       stream=None) -> None:
+        """slc_compress on the shard-local chunks [chunk_begin, chunk_begin + n_chunks) only (row f3);
+        full-shard buffers, only that range's elements / records are touched."""
+        self._check_dense(theta, theta_local, ef)
+        assert records.numel() * records.element_size() >= self.payload_bytes
+        _check(_lib.slc_compress_range(self._h, ctypes.c_int64(chunk_begin), ctypes.c_int64(n_chunks), _dptr(theta),
+                                       _dptr(theta_local), _dptr(ef), ctypes.c_float(beta), _dptr(records),
+                                       _stream_ptr(stream)), "slc_compress_range")
 
     def _peer_args(self, records: Sequence, hdrs, weights):
         R = len(records)

@@ -105,3 +105,41 @@ def test_ef_offload_needs_cuda():
     plan = slc.Plan(layouts.LAYOUTS["ragged"], device=-1)
     with pytest.raises(RuntimeError, match="CUDA"):
         EFOffload(plan)
+
+
+@pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d", "llama-tiny"])
+@pytest.mark.parametrize("nranks", [1, 3])
+@pytest.mark.parametrize("n_pieces", [1, 2, 7, 1000])
+def test_shard_pieces_cover_shard(name, nranks, n_pieces):
+    """Row f3's swap pieces: in chunk order, every chunk exactly once, disjoint increasing element ranges, and
+    every segment's elements inside the pieces (so the piecewise swap moves all of e)."""
+    from paper_2603_08163_b200 import slc
+    from paper_2603_08163_b200.offload import shard_pieces
+    for r in range(nranks):
+        plan = slc.Plan(layouts.LAYOUTS[name], rank=r, nranks=nranks, device=-1)
+        pcs = shard_pieces(plan, n_pieces)
+        c = 0
+        for c0, nc, e0, e1 in pcs:
+            assert c0 == c and nc > 0 and e1 > e0
+            c += nc
+        assert c == plan.n_chunks
+        assert all(a[3] <= b[2] for a, b in zip(pcs, pcs[1:]))
+        covered = np.zeros(plan.shard_elems, bool)
+        for _, _, e0, e1 in pcs:
+            covered[e0:e1] = True
+        for s in plan.segments:
+            assert covered[s.shard_offset:s.shard_offset + s.n_elems].all()
+        # each piece's chunk count equals the chunks its element range holds
+        for c0, nc, e0, e1 in pcs:
+            B = plan.geom.block
+            n = 0
+            for s in plan.segments:
+                lo, hi = max(e0, s.shard_offset), min(e1, s.shard_offset + s.n_elems)
+                if hi <= lo:
+                    continue
+                if s.blocked:
+                    assert (lo - s.shard_offset) % (B * s.cols) == 0
+                    n += -(-((hi - lo) // s.cols) // B) * -(-s.cols // B)
+                else:
+                    n += -(-(hi - lo) // (B * B))
+            assert n == nc

@@ -508,3 +508,34 @@ def test_ef_offload_parity(release, dtype):
     torch.cuda.synchronize()
     assert torch.equal(rec, rec2)
     assert torch.equal(off.host, ef2.cpu())
+
+
+@pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d"])
+@pytest.mark.parametrize("n_pieces", [1, 3, 16])
+def test_compress_range_and_pipelined_offload(name, n_pieces):
+    """slc_compress_range over the pieces of shard_pieces is bitwise slc_compress (chunks are independent, P:88);
+    the pipelined EF swap (row f3) gives the oracle's records and EF."""
+    from paper_2603_08163_b200.offload import EFOffload, shard_pieces
+    layout = layouts.LAYOUTS[name]
+    plan = slc.Plan(layout, dtype="f32")
+    theta, tl, ef = make_device_inputs(plan, layout, 7, 1, "f32", 4, False)
+    ef0 = ef.clone()
+    rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
+    for c0, nc, _, _ in reversed(shard_pieces(plan, n_pieces)):
+        plan.compress_range(c0, nc, theta, tl, ef, rec)
+    ref_rec, ref_ef, _ = oracle_compress_shard(plan, layout, 7, 1, "f32", 4, False)
+    assert np.array_equal(rec.cpu().numpy().view(np.uint32), ref_rec)
+    for s, e in zip(plan.segments, ref_ef):
+        assert np.array_equal(bits(seg_view(ef, s).cpu().numpy()), bits(e))
+    with pytest.raises(slc.SlcError):
+        plan.compress_range(plan.n_chunks, 1, theta, tl, ef, rec)
+    off = EFOffload(plan, n_pieces=n_pieces, release=n_pieces == 3)
+    off.host.copy_(ef0.cpu())
+    rec2 = torch.zeros_like(rec)
+    off.compress_pipelined(theta, tl, rec2)
+    off.wait()
+    torch.cuda.synchronize()
+    assert plan.get_status() == slc.OK
+    assert torch.equal(rec2, rec)
+    for s, e in zip(plan.segments, ref_ef):
+        assert np.array_equal(bits(seg_view(off.host, s).numpy()), bits(e))
