@@ -65,6 +65,7 @@ def parse():
                     help="row f3 (P:118-132): EF in pinned host memory, swapped in for compress and out every "
                          "step; serial = whole-shard swap-in, compress, swap-out overlapping the update; "
                          "pipelined (default) = per-piece H2D / compress / D2H pipeline")
+    ap.add_argument("--ef-pieces", type=int, default=16, help="pieces of the pipelined EF swap (row f3)")
     return ap.parse_args()
 
 
@@ -239,7 +240,7 @@ def run_slc(args):
     offload = None
     if args.ef_offload:
         from paper_2603_08163_b200.offload import EFOffload
-        offload = EFOffload(plan, device=dev)
+        offload = EFOffload(plan, device=dev, n_pieces=args.ef_pieces)
         offload.host.copy_(shard.ef.cpu())
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

@@ -250,6 +250,17 @@ slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payl
 /* Latched device-side status of the plan.  synchronize != 0: wait for the
  * plan's device, read and clear the device error word.  synchronize == 0:
  * return (and clear) what was already latched on the host. */
+/* NEXT row f4 (reading R#28): the enumerative index code.  For every
+ * chunk c of the shard, ranks_dev[16c .. 16c+15] (uint32, little-endian limbs,
+ * limb 0 least significant) <- sum_i binom(p_i, i + 1) over the k_eff ascending
+ * positions of record c (records_dev as written by slc_compress) — the colex
+ * rank, < binom(C_eff, k_eff), so ceil(log2 binom(C_eff, k_eff)) bits carry it
+ * (472 at C = 4096, k = 64; 7.375 bits/value against the 7.36 of P:93).
+ * Paper geometry only (C = 4096, k <= 64, 12-bit indices): UNSUPPORTED
+ * otherwise.  The first call builds a 15.7 MB binomial table on the device
+ * (owned by the plan).  4-byte aligned buffers; INVALID_ARGUMENT otherwise. */
+slc_status slc_index_rank(slc_plan* plan, const void* records_dev, uint32_t* ranks_dev, void* stream);
+
 slc_status slc_get_status(slc_plan* plan, int32_t synchronize);
 void slc_plan_destroy(slc_plan* plan);
 const char* slc_status_string(slc_status s);

@@ -40,6 +40,8 @@ struct slc_plan {
   // total, and the offset of the shard's first encoding in the message body
   int64_t* d_wire_off = nullptr;
   int64_t wire_bytes = 0, wire_offset = 0;
+  // f4 index code: binomial table binom(p, j), built on first slc_index_rank
+  uint32_t* d_binom = nullptr;
 };
 
 namespace {
@@ -602,6 +604,28 @@ slc_status slc_wire_decode(slc_plan* p, const void* wire, void* records, void* s
   return cuda_status(slc::launch_wire(a, false, static_cast<cudaStream_t>(stream)), p);
 }
 
+slc_status slc_index_rank(slc_plan* p, const void* records, uint32_t* ranks, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (!slc::index_rank_supported(p->g)) return SLC_ERR_UNSUPPORTED;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!records || !ranks || (((uintptr_t)records) & 3u) || (((uintptr_t)ranks) & 3u))
+    return SLC_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!p->d_binom) {
+    cudaError_t e = cudaMalloc(&p->d_binom, slc::binom_table_bytes(p->g));
+    if (e != cudaSuccess) {
+      p->d_binom = nullptr;
+      return cuda_status(e, p);
+    }
+    e = slc::build_binom_table(p->d_binom, p->g, st);
+    if (e != cudaSuccess) return cuda_status(e, p);
+  }
+  return cuda_status(slc::launch_index_rank(p->d_chunks, p->n_chunks, static_cast<const uint32_t*>(records),
+                                            p->d_binom, ranks, p->g, st),
+                     p);
+}
+
 static void put_be(uint8_t* o, uint64_t v, int n) {
   for (int i = 0; i < n; i++) o[i] = (uint8_t)(v >> (8 * (n - 1 - i)));
 }
@@ -659,6 +683,7 @@ void slc_plan_destroy(slc_plan* p) {
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
     if (p->d_wire_off) cudaFree(p->d_wire_off);
+    if (p->d_binom) cudaFree(p->d_binom);
   }
   delete p;
 }

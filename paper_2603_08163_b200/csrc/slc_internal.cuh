@@ -103,6 +103,13 @@ struct WireArgs {
 };
 cudaError_t launch_wire(const WireArgs& a, bool encode, cudaStream_t s);
 
+// row f4 (index_code.cu): colex rank of each chunk's index set (R#28)
+bool index_rank_supported(const Geom& g);
+size_t binom_table_bytes(const Geom& g);
+cudaError_t build_binom_table(uint32_t* T, const Geom& g, cudaStream_t s);
+cudaError_t launch_index_rank(const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* rec, const uint32_t* T,
+                              uint32_t* ranks, const Geom& g, cudaStream_t s);
+
 // launchers (return cudaGetLastError())
 cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one CTA per chunk, any compiled C (reference kernel for the pipelined one)

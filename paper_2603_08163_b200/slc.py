@@ -83,6 +83,7 @@ def _load():
         "slc_wire_decode": (ctypes.c_int, [P, P, P, P]),
         "slc_wire_header_write": (ctypes.c_int, [pp(PayloadHdr), ctypes.c_int64, P]),
         "slc_wire_header_read": (ctypes.c_int, [P, ctypes.c_int64, pp(PayloadHdr), pp(ctypes.c_int64)]),
+        "slc_index_rank": (ctypes.c_int, [P, P, P, P]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
         "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -100,7 +101,7 @@ EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_rec
             "slc_compress", "slc_compress_range", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
-            "slc_plan_destroy", "slc_status_string"]
+            "slc_plan_destroy", "slc_status_string", "slc_index_rank"]
 
 
 def status_string(s: int) -> str:
@@ -258,6 +259,12 @@ class Plan:
         _check(_lib.slc_compress_range(self._h, ctypes.c_int64(chunk_begin), ctypes.c_int64(n_chunks), _dptr(theta),
                                        _dptr(theta_local), _dptr(ef), ctypes.c_float(beta), _dptr(records),
                                        _stream_ptr(stream)), "slc_compress_range")
+
+    def index_rank(self, records, ranks, stream=None) -> None:
+        """Row f4 (R#28): colex rank of every chunk's index set, ranks: [n_chunks * 16] int32/uint32
+        little-endian limbs."""
+        assert ranks.numel() * ranks.element_size() >= self.n_chunks * 64
+        _check(_lib.slc_index_rank(self._h, _dptr(records), _dptr(ranks), _stream_ptr(stream)), "slc_index_rank")
 
     def _peer_args(self, records: Sequence, hdrs, weights):
         R = len(records)

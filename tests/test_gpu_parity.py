@@ -512,18 +512,19 @@ def test_ef_offload_parity(release, dtype):
 
 @pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d"])
 @pytest.mark.parametrize("n_pieces", [1, 3, 16])
-def test_compress_range_and_pipelined_offload(name, n_pieces):
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_compress_range_and_pipelined_offload(name, n_pieces, dtype):
     """slc_compress_range over the pieces of shard_pieces is bitwise slc_compress (chunks are independent, P:88);
     the pipelined EF swap (row f3) gives the oracle's records and EF."""
     from paper_2603_08163_b200.offload import EFOffload, shard_pieces
     layout = layouts.LAYOUTS[name]
-    plan = slc.Plan(layout, dtype="f32")
-    theta, tl, ef = make_device_inputs(plan, layout, 7, 1, "f32", 4, False)
+    plan = slc.Plan(layout, dtype=dtype)
+    theta, tl, ef = make_device_inputs(plan, layout, 7, 1, dtype, 4, False)
     ef0 = ef.clone()
     rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
     for c0, nc, _, _ in reversed(shard_pieces(plan, n_pieces)):
         plan.compress_range(c0, nc, theta, tl, ef, rec)
-    ref_rec, ref_ef, _ = oracle_compress_shard(plan, layout, 7, 1, "f32", 4, False)
+    ref_rec, ref_ef, _ = oracle_compress_shard(plan, layout, 7, 1, dtype, 4, False)
     assert np.array_equal(rec.cpu().numpy().view(np.uint32), ref_rec)
     for s, e in zip(plan.segments, ref_ef):
         assert np.array_equal(bits(seg_view(ef, s).cpu().numpy()), bits(e))
@@ -539,3 +540,35 @@ def test_compress_range_and_pipelined_offload(name, n_pieces):
     assert torch.equal(rec2, rec)
     for s, e in zip(plan.segments, ref_ef):
         assert np.array_equal(bits(seg_view(off.host, s).numpy()), bits(e))
+
+
+@pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d"])
+@pytest.mark.parametrize("special", [0, 4])
+def test_index_rank_parity(name, special):
+    """Row f4 (R#28): slc_index_rank on ORACLE records equals the oracle's colex rank of the decoded
+    positions, limb for limb; every rank fits in ceil(log2 binom(C_eff, k_eff)) bits."""
+    from oracle import index_coding as ic
+    from helpers import shard_chunk_lengths
+    layout = layouts.LAYOUTS[name]
+    plan = slc.Plan(layout, dtype="f32")
+    ref_rec, _, _ = oracle_compress_shard(plan, layout, 11, 3, "f32", special, special == 0)
+    rec = torch.from_numpy(ref_rec.view(np.uint8).copy()).to(DEV)
+    ranks = torch.full((plan.n_chunks * 16,), -1, dtype=torch.int32, device=DEV)
+    plan.index_rank(rec, ranks)
+    torch.cuda.synchronize()
+    got = ranks.cpu().numpy().view(np.uint32).reshape(plan.n_chunks, 16)
+    RW = ref_rec.size // plan.n_chunks
+    g = oracle.geom(plan.geom.block, plan.geom.k, plan.geom.index_bits)
+    for c, n in enumerate(shard_chunk_lengths(plan)):
+        pos = [int(p) for p in oracle.decode_chunk(ref_rec[c * RW:(c + 1) * RW], n, g)[0]]
+        want = ic.rank(pos, n)
+        assert want.bit_length() <= ic.code_bits(n, len(pos))
+        assert sum(int(w) << (32 * l) for l, w in enumerate(got[c])) == want, f"chunk {c}"
+
+
+def test_index_rank_unsupported_geometry():
+    plan = slc.Plan(layouts.LAYOUTS["ragged"], geom=slc.geometry(32, 16))
+    rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
+    ranks = torch.zeros(plan.n_chunks * 16, dtype=torch.int32, device=DEV)
+    with pytest.raises(slc.SlcError):
+        plan.index_rank(rec, ranks)
