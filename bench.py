@@ -65,6 +65,8 @@ def parse():
                     help="row f3 (P:118-132): EF in pinned host memory, swapped in for compress and out every "
                          "step; serial = whole-shard swap-in, compress, swap-out overlapping the update; "
                          "pipelined (default) = per-piece H2D / compress / D2H pipeline")
+    ap.add_argument("--index-code", action="store_true",
+                    help="row f4: also time slc_index_rank (colex index code, R#28) on the step's records")
     ap.add_argument("--ef-pieces", type=int, default=16, help="pieces of the pipelined EF swap (row f3)")
     return ap.parse_args()
 
@@ -359,6 +361,8 @@ def run_slc(args):
                             else 0)) * args.steps,
         "clocks": clk.summary(),
     }
+    if args.index_code:
+        out["index_code"] = time_index_rank(plan, shard, stream)
     if offload is not None:
         out["config"]["ef_offload"] = {"mode": args.ef_offload, "pieces": len(offload.pieces),
                                        **time_offload(offload, stream, reps=3)}
@@ -379,6 +383,24 @@ def run_slc(args):
     if world > 1:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def time_index_rank(plan, shard, stream, reps=5):
+    """Row f4: slc_index_rank over the shard's own records (not in the timed step)."""
+    import torch
+    ranks = torch.empty(plan.n_chunks * 16, dtype=torch.int32, device=shard.records.device)
+    plan.index_rank(shard.records, ranks, stream=stream)  # builds the binomial table once
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        plan.index_rank(shard.records, ranks, stream=stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    return {"ms": ms, "chunks": plan.n_chunks, "chunks_per_s": plan.n_chunks / (ms * 1e-3),
+            "bits_per_chunk_full": 472, "note": "R#28 colex rank; reads the 96-B index field + 64 binomial "
+            "table rows (15.7 MB table, L2-resident) per chunk, writes 64 B"}
 
 
 def time_offload(offload, stream, reps=3):
