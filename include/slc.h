@@ -257,7 +257,7 @@ slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payl
  * rank, < binom(C_eff, k_eff), so ceil(log2 binom(C_eff, k_eff)) bits carry it
  * (472 at C = 4096, k = 64; 7.375 bits/value against the 7.36 of P:93).
  * Paper geometry only (C = 4096, k <= 64, 12-bit indices): UNSUPPORTED
- * otherwise.  The first call builds a 15.7 MB binomial table on the device
+ * otherwise.  The first call builds a 16.8 MB binomial table on the device
  * (owned by the plan).  4-byte aligned buffers; INVALID_ARGUMENT otherwise. */
 slc_status slc_index_rank(slc_plan* plan, const void* records_dev, uint32_t* ranks_dev, void* stream);
 

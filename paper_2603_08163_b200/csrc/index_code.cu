@@ -7,8 +7,10 @@
 // binom(p, j), p < 4096, j <= 64, is < 2^472 = 15 32-bit limbs.
 //  * binom_table_kernel: one CTA of k threads builds the table T[p][j-1] =
 //    binom(p, j) row by row with Pascal's rule in multi-precision (4096 rows,
-//    a barrier between rows); built once per plan (15.7 MB of HBM).
-//  * index_rank_kernel: one warp per chunk; lane l adds the table entries of
+//    a barrier between rows), entries padded to 64 B; built once per plan
+//    (16.8 MB of HBM, L2-resident).
+//  * index_rank_kernel: one warp per chunk; lane l adds the table entries (four
+//    16-B loads each; 15 scalar loads made the kernel L1-bound) of
 //    positions l and l + 32 into per-limb 64-bit sums, a xor butterfly sums
 //    the lanes, lane 0 propagates the carries and writes 16 limbs.
 #include <algorithm>
@@ -18,24 +20,26 @@
 namespace slc {
 namespace {
 
-constexpr int kL = 15;  // limbs per table entry
+constexpr int kL = 15;  // limbs of a binomial
+constexpr int kS = 16;  // table stride in limbs (64 B: four 16-B loads per entry; limb 15 = 0)
 
 __global__ void __launch_bounds__(64) binom_table_kernel(uint32_t* T, int C, int K) {
   const int j = threadIdx.x + 1;  // binom(p, j)
   for (int p = 0; p < C; p++) {
-    uint32_t* out = T + ((int64_t)p * K + (j - 1)) * kL;
+    uint32_t* out = T + ((int64_t)p * K + (j - 1)) * kS;
     if (j <= K) {
       if (p == 0) {
-        for (int l = 0; l < kL; l++) out[l] = 0u;  // binom(0, j) = 0 for j >= 1
+        for (int l = 0; l < kS; l++) out[l] = 0u;  // binom(0, j) = 0 for j >= 1
       } else {
-        const uint32_t* b = T + ((int64_t)(p - 1) * K + (j - 1)) * kL;               // binom(p-1, j)
-        const uint32_t* a = j >= 2 ? T + ((int64_t)(p - 1) * K + (j - 2)) * kL : nullptr;  // binom(p-1, j-1)
+        const uint32_t* b = T + ((int64_t)(p - 1) * K + (j - 1)) * kS;               // binom(p-1, j)
+        const uint32_t* a = j >= 2 ? T + ((int64_t)(p - 1) * K + (j - 2)) * kS : nullptr;  // binom(p-1, j-1)
         uint64_t carry = 0;
         for (int l = 0; l < kL; l++) {
           const uint64_t s = (uint64_t)b[l] + (a ? a[l] : (l == 0 ? 1u : 0u)) + carry;
           out[l] = (uint32_t)s;
           carry = s >> 32;
         }
+        out[kL] = 0u;
       }
     }
     __syncthreads();
@@ -60,9 +64,15 @@ __global__ void __launch_bounds__(256) index_rank_kernel(const ChunkDesc* chunks
         const int bit = g.ib * i;
         const uint32_t p =
             __funnelshift_r(__ldg(r + (bit >> 5)), __ldg(r + (bit >> 5) + 1), bit & 31) & ((1u << g.ib) - 1u);
-        const uint32_t* t = T + ((int64_t)p * g.k + i) * kL;  // binom(p, i + 1)
+        const uint4* t = reinterpret_cast<const uint4*>(T + ((int64_t)p * g.k + i) * kS);  // binom(p, i + 1)
 #pragma unroll
-        for (int l = 0; l < kL; l++) acc[l] += __ldg(t + l);
+        for (int q = 0; q < 4; q++) {
+          const uint4 v = __ldg(t + q);
+          acc[4 * q] += v.x;
+          acc[4 * q + 1] += v.y;
+          acc[4 * q + 2] += v.z;
+          if (4 * q + 3 < kL) acc[4 * q + 3] += v.w;
+        }
       }
     }
 #pragma unroll
@@ -92,7 +102,7 @@ cudaError_t build_binom_table(uint32_t* T, const Geom& g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-size_t binom_table_bytes(const Geom& g) { return (size_t)g.C * g.k * kL * sizeof(uint32_t); }
+size_t binom_table_bytes(const Geom& g) { return (size_t)g.C * g.k * kS * sizeof(uint32_t); }
 
 cudaError_t launch_index_rank(const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* rec, const uint32_t* T,
                               uint32_t* ranks, const Geom& g, cudaStream_t s) {
