@@ -20,6 +20,12 @@
 namespace slc {
 namespace {
 
+// table loads: read-only cached (__ldg) by default; -DSLC_IC_LOAD=__ldcg (L2 only)
+// measured slower: 0.484 vs 0.444 ms on Llama-3.2-1B (the table rows of hot
+// low positions do hit in L1)
+#ifndef SLC_IC_LOAD
+#define SLC_IC_LOAD __ldg
+#endif
 constexpr int kL = 15;  // limbs of a binomial
 constexpr int kS = 16;  // table stride in limbs (64 B: four 16-B loads per entry; limb 15 = 0)
 
@@ -67,7 +73,7 @@ __global__ void __launch_bounds__(256) index_rank_kernel(const ChunkDesc* chunks
         const uint4* t = reinterpret_cast<const uint4*>(T + ((int64_t)p * g.k + i) * kS);  // binom(p, i + 1)
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          const uint4 v = __ldg(t + q);
+          const uint4 v = SLC_IC_LOAD(t + q);
           acc[4 * q] += v.x;
           acc[4 * q + 1] += v.y;
           acc[4 * q + 2] += v.z;
