@@ -52,12 +52,13 @@ __global__ void __launch_bounds__(64) binom_table_kernel(uint32_t* T, int C, int
   }
 }
 
-#ifndef SLC_IC_MINB
-#define SLC_IC_MINB 1  // min CTAs per SM; measured: 3 (80 regs, small spill) 0.453 ms vs 0.444 ms at 1 (85 regs)
+// -DSLC_IC_MINB=3 (80 regs, small spill) measured 0.453 ms vs 0.444 ms without a minimum
+#ifdef SLC_IC_MINB
+__global__ void __launch_bounds__(256, SLC_IC_MINB) index_rank_kernel(
+#else
+__global__ void __launch_bounds__(256) index_rank_kernel(
 #endif
-__global__ void __launch_bounds__(256, SLC_IC_MINB) index_rank_kernel(const ChunkDesc* chunks, int64_t n_chunks,
-                                                         const uint32_t* rec, const uint32_t* T, uint32_t* ranks,
-                                                         Geom g) {
+    const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* rec, const uint32_t* T, uint32_t* ranks, Geom g) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n_chunks; c += warps) {
