@@ -10,8 +10,10 @@ Every function follows PAPER.md §2.1 Eq. 1 / P:88 / P:93 / P:176 /
 Eq. 2; see slco.c for the step-by-step citations and DESIGN.md §3
 for the readings R#1..R#26.  Parity status: Top-k, EF identity, aggregation,
 outer update, chunking, record size and the printed closed forms are pinned by
-tests/test_oracle.py; the 2-bit quantiser Q (R#1) is "parity unpinned" by the
-paper (only SPEC's worked example and invariants pin it).
+tests/test_oracle.py and tests/test_oracle_pins.py (hand-worked cases for the
+readings the paper leaves open: Q of R#1 per SPEC S:120, the R#13 tree, the
+R#17 order and invR product, R#18 rounding); tools/oracle_mutants.py checks
+that 27 plausible slips in slco.c each fail a pin.
 """
 from __future__ import annotations
 
@@ -23,7 +25,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslco.so")
+# SLCO_LIB: a mutated build of slco.c (tools/oracle_mutants.py checks that the pins catch it)
+LIB_PATH = os.environ.get("SLCO_LIB") or os.path.join(_HERE, "libslco.so")
 SRC = os.path.join(_HERE, "slco.c")
 CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -32,6 +35,8 @@ F32, BF16 = 0, 1
 
 
 def build(force: bool = False) -> str:
+    if os.environ.get("SLCO_LIB"):
+        return LIB_PATH
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
             os.path.getmtime(SRC), os.path.getmtime(os.path.join(_HERE, "slco.h"))):
         subprocess.check_call(["gcc", *CFLAGS, "-o", LIB_PATH, SRC, "-lm"])

@@ -10,9 +10,9 @@
  * passage of /root/reference/PAPER.md (P:line) it follows; readings of points
  * the paper leaves open are the numbered ones in DESIGN.md §3 ("R#n").
  *
- * Parity pins: see tests/test_oracle.py.  Functions whose result the paper
- * does not fix (the 2-bit quantiser Q, R#1) are marked "parity unpinned"
- * below and in DESIGN.md.
+ * Parity pins: tests/test_oracle.py, tests/test_oracle_pins.py.  Q (R#1) is
+ * not defined by the paper; it is pinned to SPEC S:120's reading by
+ * hand-worked cases (tests/golden/oracle_pins.json).
  */
 #ifndef SLCO_H
 #define SLCO_H
@@ -53,7 +53,7 @@ uint16_t slco_rnbf(float x);           /* fp32 -> bfloat16, RN-even */
 
 /* Eq. 1 for one chunk: b = beta*e + (a - l); Top-k; Q; record;
  * e_new = b - decode(record).  a, l are fp32 or bf16 (dtype); e fp32.
- * Q is the 2-bit sign+bucket quantiser of R#1 — parity unpinned by the paper. */
+ * Q is the 2-bit sign+bucket quantiser of R#1 (pinned by hand-worked cases). */
 int slco_compress_chunk(const void* a, const void* l, int dtype, const float* e, int n,
                         const slco_geom* g, float beta, uint32_t* rec, float* e_new);
 /* decode one record: positions and dequantised values; returns k_eff */
