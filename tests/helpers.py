@@ -141,3 +141,31 @@ def craft_records(plan, rng, exp_lo, exp_hi, zero_frac=0.05):
                 sc.append((int(rng.integers(exp_lo, exp_hi + 1)) << 10) | int(rng.integers(0, 1024)))
         out.append(pack_record(pos, codes, sc[0], sc[1], k, ib))
     return np.concatenate(out) if out else np.zeros(0, np.uint32)
+
+
+def record_from_values(pos_vals, n, k_eff, k=64, ib=12):
+    """A record (R#6 layout) whose decoded entries are exactly {position: value}
+    (at most two distinct nonzero magnitudes; a single magnitude goes to the
+    high bucket with S_lo = 0), padded to k_eff entries with zero-valued low
+    entries at the lowest unused positions."""
+    items = sorted(pos_vals.items())
+    mags = sorted({abs(float(v)) for _, v in items if v != 0})
+    assert len(mags) <= 2 and len(items) <= k_eff
+    if len(mags) == 2:
+        lo, hi = mags
+    else:
+        lo, hi = 0.0, (mags[0] if mags else 0.0)
+    pos, codes = [], []
+    for p, v in items:
+        pos.append(p)
+        codes.append((1 if v < 0 else 0) | (2 if (abs(float(v)) == hi and hi != lo) else 0))
+    used = set(pos)
+    for p in range(n):
+        if len(pos) == k_eff:
+            break
+        if p not in used:
+            pos.append(p)
+            codes.append(0)
+    order = np.argsort(pos)
+    return pack_record(np.array(pos)[order], np.array(codes)[order], np.float16(lo).view(np.uint16),
+                       np.float16(hi).view(np.uint16), k, ib)

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
-from helpers import pack_record
+from helpers import pack_record, record_from_values
 
 G = oracle.geom()
 
@@ -212,29 +212,7 @@ def test_tree_sum_hand_worked_probes():
 
 # ---------------------------------------------------------------- weighted aggregation (R#17, R#20)
 def _rec_at(g, pos_vals, n):
-    """A record whose decoded entries are exactly pos_vals {p: value}, built with
-    the test-side packer (low bucket = 0, high bucket = |value| when all
-    nonzero magnitudes agree; else two magnitudes)."""
-    ke = oracle.effective_k(n, g)
-    items = sorted(pos_vals.items())
-    mags = sorted({abs(float(v)) for _, v in items if v != 0})
-    assert len(mags) <= 2
-    lo, hi = (0.0, mags[0]) if len(mags) == 1 else ((mags[0], mags[1]) if mags else (0.0, 0.0))
-    pos, codes = [], []
-    for p, v in items:
-        pos.append(p)
-        codes.append((1 if v < 0 else 0) | (2 if abs(float(v)) == hi and hi != lo else 0))
-    # fill up to k_eff with zero-valued low entries at unused positions
-    free = [p for p in range(n) if p not in pos_vals]
-    for p in free[:ke - len(pos)]:
-        pos.append(p)
-        codes.append(0)
-    order = np.argsort(pos)
-    pos = np.array(pos)[order]
-    codes = np.array(codes)[order]
-    if len(mags) == 1:
-        lo = 0.0
-    return pack_record(pos, codes, np.float16(lo).view(np.uint16), np.float16(hi).view(np.uint16), g.k, g.index_bits)
+    return record_from_values(pos_vals, n, oracle.effective_k(n, g), g.k, g.index_bits)
 
 
 @pytest.mark.parametrize("case", [0, 1])
