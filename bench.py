@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--index-code", action="store_true",
                     help="row f4: also time slc_index_rank (colex index code, R#28) on the step's records")
     ap.add_argument("--ef-pieces", type=int, default=16, help="pieces of the pipelined EF swap (row f3)")
+    ap.add_argument("--agg-kernel", default="auto", choices=["auto", "batch", "pipe", "simple"],
+                    help="decode / fused-update implementation (SLC_OPT_AGG_KERNEL; auto = batched where it applies)")
     return ap.parse_args()
 
 
@@ -210,6 +212,7 @@ def run_slc(args):
 
     global SPECIAL_PERIOD
     SPECIAL_PERIOD = args.special_period
+    slc.Plan.default_options = {slc.OPT_AGG_KERNEL: slc.AGG_KERNELS[args.agg_kernel]}
     rank, world, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
@@ -346,6 +349,7 @@ def run_slc(args):
         "config": {"workload": f"{wl} ({P_total} params), R={R} peers, C={args.block ** 2} k={args.k} 2-bit, "
                                f"beta={BETA} alpha={ALPHA}",
                    "params": P_total, "peers": R, "parallelism": f"fsdp-shard{world}",
+                   "agg_kernel": args.agg_kernel,
                    "l2": "inputs > L2 (126 MB): no flush needed"},
         "hbm_gbs": step_gbs_rank * world,
         "hbm_frac_of_peak": step_gbs_rank / peak,
@@ -451,22 +455,34 @@ def time_collectives(plan, gather, shard, R, stream, dev, reps=5):
     ag_ms = a.elapsed_time(b) / reps
     ex = sdist.PeerExchange(gather, R)
     owned = [gather.message for _ in range(rank, R, world)]  # every peer message: same bytes, same size
-    ex.run(owned)
-    torch.cuda.synchronize()
-    dist.barrier()
-    a.record(stream)
-    for _ in range(reps):
-        ex.run(owned)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ex_ms = a.elapsed_time(b) / reps
-    t = torch.tensor([ag_ms, ex_ms], dtype=torch.float64, device=dev)
+    for i, m in enumerate(owned):
+        ex.stage(i, m)  # where the download would have written them
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    ex_ms = timed(ex.exchange)
+    p2p_ms = timed(lambda: ex.run_p2p(owned))
+    del ex
+    t = torch.tensor([ag_ms, ex_ms, p2p_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ag_ms, ex_ms = t.tolist()
+    ag_ms, ex_ms, p2p_ms = t.tolist()
+    moved = R * plan.payload_bytes * (world - 1) / world  # bytes per rank that cross NVLink
     msg = sum(gather.sizes)
     return {"allgather_ms": ag_ms, "allgather_message_bytes": msg,
             "allgather_busbw_gbs": msg * (world - 1) / world / (ag_ms * 1e-3) / 1e9,
             "exchange_ms": ex_ms, "exchange_bytes_per_rank": R * plan.payload_bytes,
+            "exchange_gbs_per_rank": moved / (ex_ms * 1e-3) / 1e9,
+            "exchange_p2p_ms": p2p_ms, "exchange_method": "staged all_to_all_single (one NCCL call); "
+                                                          "p2p = grouped send/recv per (peer, dst) slice",
             "note": "all-gather overlapped with the fused update inside the step; exchange (stand-in for the "
                     "R2 download) reported separately, not in ms_per_step"}
 

@@ -18,13 +18,16 @@
  *  - Compute calls are asynchronous on `stream` (a cudaStream_t passed as
  *    void*, NULL = legacy default stream), allocate nothing and never
  *    synchronize.  One plan must not be used on two streams concurrently.
+ *    The plan remembers the stream of its most recent call (for
+ *    slc_get_status); that stream must outlive the call to slc_get_status.
  *  - Argument / header errors are detected on the host and returned
  *    synchronously; nothing is launched then.  Data errors found on the device
  *    (a non-finite theta, theta_local, e or beta*e + Delta; an fp16 scale that
  *    overflows) are LATCHED in the plan and reported by slc_get_status(); the
  *    outputs of the offending call are then unspecified.
- *  - The only allocations are made by slc_plan_create (device chunk table and
- *    error word) and released by slc_plan_destroy.
+ *  - Allocations are made only by slc_plan_create (device chunk table, wire
+ *    offsets and error word) and by slc_plan_set_option(SLC_OPT_INDEX_CODE)
+ *    (the f4 binomial table); slc_plan_destroy releases them.
  */
 #ifndef SLC_H
 #define SLC_H
@@ -232,7 +235,9 @@ slc_status slc_outer_update_wdev(slc_plan* plan, void* theta_dev, const slc_payl
  *   body_offset bytes after the header.
  * slc_wire_encode: records_dev (this shard's records, slc_compress layout) ->
  *   wire_dev[body_bytes] (device).  Asynchronous on stream.
- * slc_wire_decode: wire_dev[body_bytes] -> records_dev, validating every chunk
+ * slc_wire_decode: wire_dev[nbytes] -> records_dev; nbytes < body_bytes (a
+ *   truncated body) returns SLC_ERR_FORMAT and reads nothing; else
+ *   the first body_bytes bytes are decoded, validating every chunk
  *   (count == k_eff, indices strictly increasing and < the chunk length, zero
  *   padding, scales finite, >= 0, lo <= hi); a violation latches
  *   SLC_ERR_INVALID_DATA (reported by slc_get_status) and zeroes that record.
@@ -242,14 +247,11 @@ slc_status slc_outer_update_wdev(slc_plan* plan, void* theta_dev, const slc_payl
  *   not on the wire: the caller's plan supplies them). */
 slc_status slc_wire_layout(const slc_plan* plan, int64_t* body_bytes_host, int64_t* body_offset_host);
 slc_status slc_wire_encode(slc_plan* plan, const void* records_dev, void* wire_dev, void* stream);
-slc_status slc_wire_decode(slc_plan* plan, const void* wire_dev, void* records_dev, void* stream);
+slc_status slc_wire_decode(slc_plan* plan, const void* wire_dev, int64_t nbytes, void* records_dev, void* stream);
 slc_status slc_wire_header_write(const slc_payload_hdr* hdr_host, int64_t total_chunks, uint8_t out_host[65]);
 slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payload_hdr* hdr_host,
                                 int64_t* total_chunks_host);
 
-/* Latched device-side status of the plan.  synchronize != 0: wait for the
- * plan's device, read and clear the device error word.  synchronize == 0:
- * return (and clear) what was already latched on the host. */
 /* NEXT row f4 (reading R#28): the enumerative index code.  For every
  * chunk c of the shard, ranks_dev[16c .. 16c+15] (uint32, little-endian limbs,
  * limb 0 least significant) <- sum_i binom(p_i, i + 1) over the k_eff ascending
@@ -257,10 +259,33 @@ slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payl
  * rank, < binom(C_eff, k_eff), so ceil(log2 binom(C_eff, k_eff)) bits carry it
  * (472 at C = 4096, k = 64; 7.375 bits/value against the 7.36 of P:93).
  * Paper geometry only (C = 4096, k <= 64, 12-bit indices): UNSUPPORTED
- * otherwise.  The first call builds a 16.8 MB binomial table on the device
- * (owned by the plan).  4-byte aligned buffers; INVALID_ARGUMENT otherwise. */
+ * otherwise.  Needs the plan's binomial table: slc_plan_set_option(plan,
+ * SLC_OPT_INDEX_CODE, 1) first (INVALID_ARGUMENT otherwise).  4-byte aligned
+ * buffers; INVALID_ARGUMENT otherwise. */
 slc_status slc_index_rank(slc_plan* plan, const void* records_dev, uint32_t* ranks_dev, void* stream);
 
+/* Plan options (configuration calls: synchronous, may allocate).
+ *  SLC_OPT_AGG_KERNEL    which decode / fused-update implementation runs:
+ *                        0 auto (default: the persistent pipelined kernel
+ *                        where it applies, else one CTA per chunk), 1 the
+ *                        TMA-tile kernel (fused update, C = 4096, k = 64,
+ *                        12-bit indices, R <= 64, 16-B aligned records; else
+ *                        as 0), 2 pipelined, 3 one CTA per chunk.  Results are
+ *                        bitwise identical; the parity tests run all of them.
+ *  SLC_OPT_AGG_GRID_CAP  > 0: at most this many CTAs for the persistent decode
+ *                        kernels (every CTA then walks many chunks; test aid).
+ *  SLC_OPT_INDEX_CODE    1: build the f4 binomial table (C(p, j), p < 4096,
+ *                        j <= 64; 16.8 MB on the plan's device, synchronously);
+ *                        0: free it.  UNSUPPORTED off the paper geometry.
+ * INVALID_ARGUMENT for an unknown option or value. */
+typedef enum { SLC_OPT_AGG_KERNEL = 1, SLC_OPT_AGG_GRID_CAP = 2, SLC_OPT_INDEX_CODE = 3 } slc_option;
+slc_status slc_plan_set_option(slc_plan* plan, int32_t option, int64_t value);
+
+/* Latched status of the plan, cleared by the call.  synchronize != 0: the
+ * device error word is read and cleared on the stream of the plan's most
+ * recent call, which is then synchronized (not the whole device);
+ * synchronize == 0: only what was latched on the host (argument-time and
+ * launch errors). */
 slc_status slc_get_status(slc_plan* plan, int32_t synchronize);
 void slc_plan_destroy(slc_plan* plan);
 const char* slc_status_string(slc_status s);

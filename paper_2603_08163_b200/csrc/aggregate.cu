@@ -21,7 +21,6 @@
 // one warp walks the peers sequentially (no atomics, deterministic).
 #include <cuda_fp16.h>
 
-#include <cstdlib>
 #include <cstring>
 
 #include "chunk_io.cuh"
@@ -215,13 +214,16 @@ cudaError_t launch_one(const AggArgs& a, cudaStream_t s) {
 
 cudaError_t launch_aggregate(const AggArgs& a, int bf16, cudaStream_t s) {
   if (a.n_chunks == 0) return cudaSuccess;
-  // the persistent pipelined kernel (aggregate_pipe.cu) serves decode and fused
-  // update; SLC_AGG_KERNEL=simple selects this file's one-CTA-per-chunk kernel
-  // (kept as the second implementation the parity tests run)
-  const char* knob = std::getenv("SLC_AGG_KERNEL");
-  const bool simple = knob && std::strcmp(knob, "simple") == 0;
-  if (!simple && a.mode != kUpdateFromAgg && aggregate_pipe_supported(a) && !(bf16 && a.mode == kAggOnly))
-    return launch_aggregate_pipe(a, bf16, s);
+  // decode / fused update: the persistent pipelined kernel (aggregate_pipe.cu)
+  // by default, else this file's one-CTA-per-chunk kernel.  SLC_OPT_AGG_KERNEL
+  // (slc_plan_set_option) pins one of them, or the TMA-tile kernel
+  // (aggregate_batch.cu: fused update only, paper geometry; measured slower than
+  // the pipelined one on B200) — the parity tests run all of them.
+  if (a.mode != kUpdateFromAgg) {
+    if (a.variant == 1 && aggregate_batch_supported(a)) return launch_aggregate_batch(a, bf16, s);
+    if (a.variant != 3 && aggregate_pipe_supported(a) && !(bf16 && a.mode == kAggOnly))
+      return launch_aggregate_pipe(a, bf16, s);
+  }
   switch (a.g.C) {
     case 1024: return bf16 ? launch_one<1024, true>(a, s) : launch_one<1024, false>(a, s);
     case 4096: return bf16 ? launch_one<4096, true>(a, s) : launch_one<4096, false>(a, s);

@@ -33,7 +33,6 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "chunk_io.cuh"
 
@@ -637,8 +636,8 @@ cudaError_t launch_pipe(const AggArgs& a, cudaStream_t s) {
     return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = std::min<int64_t>(a.n_chunks, (int64_t)sms * per_sm);
-  // test knob: cap the grid so that every CTA walks many chunks (pipeline hand-offs)
-  if (const char* cap = std::getenv("SLC_AGG_GRID")) grid = std::max<int64_t>(1, std::min<int64_t>(grid, atoll(cap)));
+  // SLC_OPT_AGG_GRID_CAP: every CTA walks many chunks (pipeline hand-offs under test)
+  if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
   kern<<<(unsigned)grid, PipeCfg<C>::NT, smem, s>>>(a);
   return cudaGetLastError();
 }

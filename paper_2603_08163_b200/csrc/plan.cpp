@@ -34,14 +34,23 @@ struct slc_plan {
   std::vector<CUtensorMap> h_tmaps;
   CUtensorMap* d_tmaps = nullptr;
   const void* tmap_ptrs[3] = {nullptr, nullptr, nullptr};
+  // fused outer update: one tensor map per blocked segment over theta (tiles in / out)
+  std::vector<CUtensorMap> h_utmaps;
+  CUtensorMap* d_utmaps = nullptr;
+  const void* utmap_ptr = nullptr;
   slc_status latched = SLC_OK;
   uint8_t digest[32];
   // f2 wire format: per-chunk byte offsets of the shard's encodings, their
   // total, and the offset of the shard's first encoding in the message body
   int64_t* d_wire_off = nullptr;
   int64_t wire_bytes = 0, wire_offset = 0;
-  // f4 index code: binomial table binom(p, j), built on first slc_index_rank
+  // f4 index code: binomial table binom(p, j), built by slc_plan_set_option(SLC_OPT_INDEX_CODE)
   uint32_t* d_binom = nullptr;
+  // slc_plan_set_option
+  int agg_variant = 0;
+  int64_t agg_grid_cap = 0;
+  // stream of the most recent compute call (slc_get_status(synchronize) waits on it)
+  cudaStream_t last_stream = nullptr;
 };
 
 namespace {
@@ -174,6 +183,8 @@ slc_status prep_agg(slc_plan* p, const slc_payload_hdr* hdrs, const void* const*
   a.rec_al16 = 1;
   a.err = p->d_err;
   a.g = p->g;
+  a.variant = p->agg_variant;
+  a.grid_cap = p->agg_grid_cap;
   for (int i = 0; i < R; i++) {
     const int r = order[i];  // canonical order (matters only when weighted)
     if (!recs[r] && p->n_chunks > 0) return SLC_ERR_INVALID_ARGUMENT;
@@ -194,6 +205,11 @@ slc_status cuda_status(cudaError_t e, slc_plan* p) {
 }
 
 bool aligned16(const void* q) { return (((uintptr_t)q) & 15u) == 0; }
+
+cudaStream_t use_stream(slc_plan* p, void* stream) {
+  p->last_stream = static_cast<cudaStream_t>(stream);
+  return p->last_stream;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -240,6 +256,47 @@ cudaError_t ensure_tmaps(slc_plan* p, const void* theta, const void* theta_local
   p->tmap_ptrs[1] = theta_local;
   p->tmap_ptrs[2] = ef;
   return cudaSuccess;
+}
+
+// (re)encode the 64x64-box tensor maps over theta of every blocked segment
+// (the fused update's tile loads / stores); cached per theta pointer
+cudaError_t ensure_update_tmaps(slc_plan* p, const void* theta, cudaStream_t stream) {
+  if (p->blk_segs.empty() || p->utmap_ptr == theta) return cudaSuccess;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const int B = p->geom.block;
+  const int esz = p->dtype == SLC_BF16 ? 2 : 4;
+  const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  for (size_t i = 0; i < p->blk_segs.size(); i++) {
+    const slc_segment& s = p->segs[p->blk_segs[i]];
+    char* base = (char*)theta + (size_t)s.shard_offset * esz;
+    const cuuint64_t dims[2] = {(cuuint64_t)s.cols, (cuuint64_t)s.rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)s.cols * esz};
+    const cuuint32_t box[2] = {(cuuint32_t)B, (cuuint32_t)B};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&p->h_utmaps[i], dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaMemcpyAsync(p->d_utmaps, p->h_utmaps.data(), p->h_utmaps.size() * sizeof(CUtensorMap),
+                                  cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  p->utmap_ptr = theta;
+  return cudaSuccess;
+}
+
+// the fused update's theta tensor maps for this call (falls back to the other
+// kernels, tmaps_ok = 0, if they cannot be encoded)
+void set_update_tmaps(slc_plan* p, const void* theta, cudaStream_t stream, slc::AggArgs& a) {
+  if (p->blk_segs.empty()) {
+    a.tmaps = nullptr;
+    a.tmaps_ok = 1;
+    return;
+  }
+  const bool ok = ((uintptr_t)theta & 15u) == 0 && ensure_update_tmaps(p, theta, stream) == cudaSuccess;
+  if (!ok) cudaGetLastError();
+  a.tmaps = p->d_utmaps;
+  a.tmaps_ok = ok ? 1 : 0;
 }
 
 }  // namespace
@@ -386,6 +443,8 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
   if (ce == cudaSuccess && !p->blk_segs.empty()) {
     p->h_tmaps.resize(3 * p->blk_segs.size());
     ce = cudaMalloc(&p->d_tmaps, p->h_tmaps.size() * sizeof(CUtensorMap));
+    p->h_utmaps.resize(p->blk_segs.size());
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_utmaps, p->h_utmaps.size() * sizeof(CUtensorMap));
   }
   if (ce == cudaSuccess && !table.empty()) {
     ce = cudaMalloc(&p->d_chunks, table.size() * sizeof(ChunkDesc));
@@ -400,6 +459,7 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
+    if (p->d_utmaps) cudaFree(p->d_utmaps);
     delete p;
     cudaGetLastError();
     return SLC_ERR_CUDA;
@@ -458,7 +518,7 @@ slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* t
   a.max_ld = p->max_ld;
   a.g = p->g;
   DeviceGuard guard(p->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStream_t st = use_stream(p, stream);
   if (slc::compress_tma_supported(p->g)) {
     cudaError_t e = ensure_tmaps(p, theta, theta_local, ef, st);
     if (e != cudaSuccess) return cuda_status(e, p);
@@ -478,7 +538,7 @@ slc_status slc_decode_aggregate(slc_plan* p, const slc_payload_hdr* hdrs, const 
   a.mode = slc::kAggOnly;
   a.agg = agg;
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, use_stream(p, stream)), p);
 }
 
 slc_status slc_outer_update(slc_plan* p, void* theta, const float* agg, const slc_payload_hdr* hdrs,
@@ -504,7 +564,9 @@ slc_status slc_outer_update(slc_plan* p, void* theta, const float* agg, const sl
   a.alpha = alpha;
   a.theta = theta;
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+  cudaStream_t cs = use_stream(p, stream);
+  if (a.mode == slc::kFused) set_update_tmaps(p, theta, cs, a);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, cs), p);
 }
 
 slc_status slc_decode_aggregate_wdev(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
@@ -520,7 +582,7 @@ slc_status slc_decode_aggregate_wdev(slc_plan* p, const slc_payload_hdr* hdrs, c
   a.mode = slc::kAggOnly;
   a.agg = agg;
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, use_stream(p, stream)), p);
 }
 
 slc_status slc_outer_update_wdev(slc_plan* p, void* theta, const slc_payload_hdr* hdrs, const void* const* recs,
@@ -537,7 +599,9 @@ slc_status slc_outer_update_wdev(slc_plan* p, void* theta, const slc_payload_hdr
   a.alpha = alpha;
   a.theta = theta;
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, static_cast<cudaStream_t>(stream)), p);
+  cudaStream_t cs = use_stream(p, stream);
+  set_update_tmaps(p, theta, cs, a);
+  return cuda_status(slc::launch_aggregate(a, p->dtype == SLC_BF16, cs), p);
 }
 
 slc_status slc_payload_sqnorm(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
@@ -550,7 +614,7 @@ slc_status slc_payload_sqnorm(slc_plan* p, const slc_payload_hdr* hdrs, const vo
   for (int r = 0; r < R; r++) a.rec[r] = static_cast<const uint32_t*>(recs[r]);
   DeviceGuard guard(p->device);
   return cuda_status(slc::launch_payload_sqnorm(a, reinterpret_cast<unsigned long long*>(sqnorm_dev),
-                                                static_cast<cudaStream_t>(stream)),
+                                                use_stream(p, stream)),
                      p);
 }
 
@@ -560,7 +624,7 @@ slc_status slc_median_norm_weights(slc_plan* p, int32_t R, const uint64_t* sqnor
     return SLC_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(p->device);
   return cuda_status(slc::launch_median_weights(reinterpret_cast<const unsigned long long*>(sqnorm_dev), R,
-                                                weights_dev, norms_dev, static_cast<cudaStream_t>(stream)),
+                                                weights_dev, norms_dev, use_stream(p, stream)),
                      p);
 }
 
@@ -590,40 +654,70 @@ slc_status slc_wire_encode(slc_plan* p, const void* records, void* wire, void* s
   a.rec = static_cast<const uint32_t*>(records);
   a.wire = static_cast<uint8_t*>(wire);
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_wire(a, true, static_cast<cudaStream_t>(stream)), p);
+  return cuda_status(slc::launch_wire(a, true, use_stream(p, stream)), p);
 }
 
-slc_status slc_wire_decode(slc_plan* p, const void* wire, void* records, void* stream) {
+slc_status slc_wire_decode(slc_plan* p, const void* wire, int64_t nbytes, void* records, void* stream) {
   if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (nbytes < p->wire_bytes) return SLC_ERR_FORMAT;  // truncated body: nothing is read
   if (p->n_chunks == 0) return SLC_OK;
   if (!records || !wire || (((uintptr_t)records) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
   slc::WireArgs a = wire_args(p);
   a.wire_in = static_cast<const uint8_t*>(wire);
   a.rec_out = static_cast<uint32_t*>(records);
   DeviceGuard guard(p->device);
-  return cuda_status(slc::launch_wire(a, false, static_cast<cudaStream_t>(stream)), p);
+  return cuda_status(slc::launch_wire(a, false, use_stream(p, stream)), p);
 }
 
 slc_status slc_index_rank(slc_plan* p, const void* records, uint32_t* ranks, void* stream) {
   if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
   if (!slc::index_rank_supported(p->g)) return SLC_ERR_UNSUPPORTED;
   if (p->n_chunks == 0) return SLC_OK;
+  if (!p->d_binom) return SLC_ERR_INVALID_ARGUMENT;  // slc_plan_set_option(SLC_OPT_INDEX_CODE, 1) first
   if (!records || !ranks || (((uintptr_t)records) & 3u) || (((uintptr_t)ranks) & 3u))
     return SLC_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(p->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!p->d_binom) {
-    cudaError_t e = cudaMalloc(&p->d_binom, slc::binom_table_bytes(p->g));
-    if (e != cudaSuccess) {
-      p->d_binom = nullptr;
-      return cuda_status(e, p);
-    }
-    e = slc::build_binom_table(p->d_binom, p->g, st);
-    if (e != cudaSuccess) return cuda_status(e, p);
-  }
   return cuda_status(slc::launch_index_rank(p->d_chunks, p->n_chunks, static_cast<const uint32_t*>(records),
-                                            p->d_binom, ranks, p->g, st),
+                                            p->d_binom, ranks, p->g, use_stream(p, stream)),
                      p);
+}
+
+slc_status slc_plan_set_option(slc_plan* p, int32_t option, int64_t value) {
+  if (!p) return SLC_ERR_INVALID_ARGUMENT;
+  switch (option) {
+    case SLC_OPT_AGG_KERNEL:
+      if (value < 0 || value > 3) return SLC_ERR_INVALID_ARGUMENT;
+      p->agg_variant = (int)value;
+      return SLC_OK;
+    case SLC_OPT_AGG_GRID_CAP:
+      if (value < 0) return SLC_ERR_INVALID_ARGUMENT;
+      p->agg_grid_cap = value;
+      return SLC_OK;
+    case SLC_OPT_INDEX_CODE: {
+      if (value != 0 && value != 1) return SLC_ERR_INVALID_ARGUMENT;
+      if (p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+      DeviceGuard guard(p->device);
+      if (value == 0) {
+        if (p->d_binom) cudaFree(p->d_binom);
+        p->d_binom = nullptr;
+        return SLC_OK;
+      }
+      if (!slc::index_rank_supported(p->g)) return SLC_ERR_UNSUPPORTED;
+      if (p->d_binom) return SLC_OK;
+      uint32_t* T = nullptr;
+      cudaError_t e = cudaMalloc(&T, slc::binom_table_bytes(p->g));
+      if (e == cudaSuccess) e = slc::build_binom_table(T, p->g, nullptr);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+      if (e != cudaSuccess) {
+        if (T) cudaFree(T);
+        cudaGetLastError();
+        return SLC_ERR_CUDA;
+      }
+      p->d_binom = T;
+      return SLC_OK;
+    }
+  }
+  return SLC_ERR_INVALID_ARGUMENT;
 }
 
 static void put_be(uint8_t* o, uint64_t v, int n) {
@@ -664,11 +758,14 @@ slc_status slc_get_status(slc_plan* p, int32_t synchronize) {
   slc_status st = p->latched;
   p->latched = SLC_OK;
   if (synchronize && p->device >= 0) {
+    // read and clear the device error word on the stream of the plan's last
+    // call (stream order puts it after that call's kernels), then wait for it
     DeviceGuard guard(p->device);
     uint32_t err = 0;
-    cudaError_t ce = cudaDeviceSynchronize();
-    if (ce == cudaSuccess) ce = cudaMemcpy(&err, p->d_err, sizeof(err), cudaMemcpyDeviceToHost);
-    if (ce == cudaSuccess) ce = cudaMemset(p->d_err, 0, sizeof(uint32_t));
+    cudaStream_t s = p->last_stream;
+    cudaError_t ce = cudaMemcpyAsync(&err, p->d_err, sizeof(err), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(p->d_err, 0, sizeof(uint32_t), s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) return SLC_ERR_CUDA;
     if (err && st == SLC_OK) st = SLC_ERR_INVALID_DATA;
   }
@@ -682,6 +779,7 @@ void slc_plan_destroy(slc_plan* p) {
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
+    if (p->d_utmaps) cudaFree(p->d_utmaps);
     if (p->d_wire_off) cudaFree(p->d_wire_off);
     if (p->d_binom) cudaFree(p->d_binom);
   }

@@ -87,6 +87,10 @@ struct AggArgs {
   void* theta;    // kUpdateFromAgg / kFused: in-out
   uint32_t* err;
   Geom g;
+  int variant;       // SLC_OPT_AGG_KERNEL: 0 auto, 1 batched, 2 pipelined, 3 one CTA per chunk
+  int64_t grid_cap;  // SLC_OPT_AGG_GRID_CAP: > 0 caps the persistent kernels' grid (test aid)
+  const void* tmaps;  // fused update: CUtensorMap per blocked segment over theta (ChunkDesc.tmap)
+  int tmaps_ok;       // tmaps valid for this call's theta (always 1 without blocked segments)
 };
 
 // f2 wire format (wire.cu)
@@ -125,6 +129,9 @@ cudaError_t launch_aggregate(const AggArgs& a, int param_bf16, cudaStream_t s);
 // persistent software-pipelined decode / fused update (C = 1024, 4096)
 cudaError_t launch_aggregate_pipe(const AggArgs& a, int param_bf16, cudaStream_t s);
 bool aggregate_pipe_supported(const AggArgs& a);
+// contiguous chunk ranges, bulk-copied record batches, value tables (C = 4096, k = 64, 12-bit, R <= 64)
+cudaError_t launch_aggregate_batch(const AggArgs& a, int param_bf16, cudaStream_t s);
+bool aggregate_batch_supported(const AggArgs& a);
 // median-norm: exact per-peer squared norms as 4 un-carried 32-bit limbs per peer; weights
 cudaError_t launch_payload_sqnorm(const AggArgs& a, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_median_weights(const unsigned long long* limbs, int R, float* w, double* norms, cudaStream_t s);

@@ -12,8 +12,9 @@ into the peer message, and to exchange simulated peers' payloads").
   buffer.  The gather runs on NCCL's stream and overlaps the fused
   aggregate/update kernel, which only needs the rank's own slices.
 * a9, PeerExchange — stand-in for the R2 download: peer r's full
-  message sits on rank r % n "as if downloaded"; grouped send/recv hands every
-  rank its contiguous slice of every message.  Reported separately.
+  message sits on rank r % n "as if downloaded", staged so that what each
+  destination needs is contiguous; one all-to-all hands every rank its slice
+  of every message.  Reported separately.
 
 No dense tensor ever crosses NVLink.  Works with the gloo backend on CPU
 tensors too (tests/test_dist_cpu.py).
@@ -72,20 +73,59 @@ class PayloadGather:
 
 class PeerExchange:
     """a9: peer r's (padded) message lives on rank r % n; every rank receives
-    its own slice of every message.  Returns per-peer slice buffers."""
+    its own slice of every message.
+
+    The owned messages are staged (as the download would write them) in a
+    [dst rank][owned peer][slot] buffer, so that the part every destination
+    needs is one contiguous range, and ONE ncclAllToAll-style call
+    (all_to_all_single with per-rank split sizes) moves every (peer, dst)
+    slice at once; it lands in a [src rank][owned peer of src][slot] buffer.
+    `run_p2p` is the earlier grouped send/recv version (one op per (peer,
+    dst) pair), kept for comparison in bench.py's collectives report."""
 
     def __init__(self, gather: PayloadGather, n_peers: int):
         self.g = gather
         self.n_peers = n_peers
+        world, rank, slot = gather.world, gather.rank, gather.slot
         dev = gather.message.device
-        self.slices = [torch.zeros(gather.slot, dtype=torch.uint8, device=dev) for _ in range(n_peers)]
+        self.n_own = [len(range(g, n_peers, world)) for g in range(world)]
+        self.send = torch.zeros(world * self.n_own[rank] * slot, dtype=torch.uint8, device=dev)
+        self.recv = torch.zeros(n_peers * slot, dtype=torch.uint8, device=dev)
+        self._roff = [sum(self.n_own[:g]) * slot for g in range(world)]
+        self.slices = None  # run_p2p's receive buffers, allocated on first use
 
     def owner(self, r: int) -> int:
         return r % self.g.world
 
+    def stage(self, i: int, message: torch.Tensor):
+        """Place owned peer i's full padded message (peer r = rank + i*world) in the send buffer."""
+        world, slot, no = self.g.world, self.g.slot, self.n_own[self.g.rank]
+        self.send.view(world, no, slot)[:, i, :].copy_(message.view(world, slot))
+
+    def exchange(self):
+        """The one collective: every rank gets its slice of every peer's message."""
+        world, rank, slot = self.g.world, self.g.rank, self.g.slot
+        dist.all_to_all_single(self.recv, self.send, output_split_sizes=[n * slot for n in self.n_own],
+                               input_split_sizes=[self.n_own[rank] * slot] * world, group=self.g.group)
+
+    def slice(self, r: int) -> torch.Tensor:
+        """Peer r's slice for this rank (a view into the receive buffer)."""
+        src, i = r % self.g.world, r // self.g.world
+        o = self._roff[src] + i * self.g.slot
+        return self.recv[o:o + self.g.sizes[self.g.rank]]
+
     def run(self, owned_messages: Sequence[torch.Tensor]):
         """owned_messages[i] = full padded message of peer r = rank + i*world."""
+        for i, m in enumerate(owned_messages):
+            self.stage(i, m)
+        self.exchange()
+        return [self.slice(r) for r in range(self.n_peers)]
+
+    def run_p2p(self, owned_messages: Sequence[torch.Tensor]):
+        """Grouped send/recv, one op per (peer, destination) slice."""
         world, rank, slot = self.g.world, self.g.rank, self.g.slot
+        if self.slices is None:
+            self.slices = [torch.zeros(slot, dtype=torch.uint8, device=self.recv.device) for _ in range(self.n_peers)]
         ops = []
         for r in range(self.n_peers):
             o = self.owner(r)
@@ -129,7 +169,12 @@ class MedianNorm:
         return limbs
 
     def __call__(self, records: Sequence[torch.Tensor], hdrs=None, stream=None) -> torch.Tensor:
-        self.plan.payload_sqnorm(records, self.limbs, hdrs=hdrs, stream=stream)
-        self.reduce_limbs(self.limbs)
-        self.plan.median_norm_weights(self.limbs, self.weights, self.norms, stream=stream)
+        # the all-reduce is ordered on torch's current stream: run the whole
+        # sequence (sqnorm kernel -> all-reduce -> weights kernel) on `stream`
+        # made current, so each step sees the previous one's result
+        s = stream if stream is not None else torch.cuda.current_stream(self.limbs.device)
+        with torch.cuda.stream(s):
+            self.plan.payload_sqnorm(records, self.limbs, hdrs=hdrs, stream=s)
+            self.reduce_limbs(self.limbs)
+            self.plan.median_norm_weights(self.limbs, self.weights, self.norms, stream=s)
         return self.weights

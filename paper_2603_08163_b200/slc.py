@@ -80,10 +80,11 @@ def _load():
         "slc_outer_update_wdev": (ctypes.c_int, [P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
         "slc_wire_layout": (ctypes.c_int, [P, pp(ctypes.c_int64), pp(ctypes.c_int64)]),
         "slc_wire_encode": (ctypes.c_int, [P, P, P, P]),
-        "slc_wire_decode": (ctypes.c_int, [P, P, P, P]),
+        "slc_wire_decode": (ctypes.c_int, [P, P, ctypes.c_int64, P, P]),
         "slc_wire_header_write": (ctypes.c_int, [pp(PayloadHdr), ctypes.c_int64, P]),
         "slc_wire_header_read": (ctypes.c_int, [P, ctypes.c_int64, pp(PayloadHdr), pp(ctypes.c_int64)]),
         "slc_index_rank": (ctypes.c_int, [P, P, P, P]),
+        "slc_plan_set_option": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int64]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
         "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -101,7 +102,11 @@ EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_rec
             "slc_compress", "slc_compress_range", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
-            "slc_plan_destroy", "slc_status_string", "slc_index_rank"]
+            "slc_plan_destroy", "slc_status_string", "slc_index_rank", "slc_plan_set_option"]
+
+# slc_option (include/slc.h)
+OPT_AGG_KERNEL, OPT_AGG_GRID_CAP, OPT_INDEX_CODE = 1, 2, 3
+AGG_KERNELS = {"auto": 0, "batch": 1, "pipe": 2, "simple": 3}
 
 
 def status_string(s: int) -> str:
@@ -200,7 +205,12 @@ def make_header(plan: "Plan", peer_id: bytes, base_round: int = 0) -> PayloadHdr
 
 class Plan:
     """slc_plan of shard `rank` of `nranks` of a global layout.  device < 0 ->
-    host-only plan (geometry / partition queries, no compute)."""
+    host-only plan (geometry / partition queries, no compute).
+
+    `default_options` ({slc_option: value}) is applied to every new device
+    plan (the tests use it to pin one decode implementation)."""
+
+    default_options: dict = {}
 
     def __init__(self, layout, geom: Optional[Geometry] = None, rank: int = 0, nranks: int = 1,
                  dtype: str = "f32", device: int = 0):
@@ -223,6 +233,14 @@ class Plan:
             _check(_lib.slc_plan_segment(h, i, ctypes.byref(s)), "slc_plan_segment")
             self.segments.append(SegmentInfo(s.tensor, bool(s.blocked), s.tensor_begin, s.n_elems, s.shard_offset,
                                              s.rows, s.cols, s.first_chunk, s.n_chunks))
+        self._index_code = False
+        if device >= 0:
+            for opt, val in Plan.default_options.items():
+                self.set_option(opt, val)
+
+    def set_option(self, option: int, value: int) -> None:
+        """slc_plan_set_option (OPT_AGG_KERNEL / OPT_AGG_GRID_CAP / OPT_INDEX_CODE)."""
+        _check(_lib.slc_plan_set_option(self._h, int(option), int(value)), "slc_plan_set_option")
 
     # ---- shape helpers
     @property
@@ -246,7 +264,7 @@ class Plan:
         """Eq. 1 (P:68-75).  theta/theta_local: [shard_elems] f32|bf16, ef: [shard_elems] f32 (in place),
         records: [payload_bytes] uint8 (or any 4-byte aligned buffer of that size)."""
         self._check_dense(theta, theta_local, ef)
-        assert records.numel() * records.element_size() >= self.payload_bytes
+        self._check_bytes(records, self.payload_bytes, "records")
         _check(_lib.slc_compress(self._h, _dptr(theta), _dptr(theta_local), _dptr(ef), ctypes.c_float(beta),
                                  _dptr(records), _stream_ptr(stream)), "slc_compress")
 
@@ -255,21 +273,27 @@ class Plan:
         """slc_compress on the shard-local chunks [chunk_begin, chunk_begin + n_chunks) only (row f3);
         full-shard buffers, only that range's elements / records are touched."""
         self._check_dense(theta, theta_local, ef)
-        assert records.numel() * records.element_size() >= self.payload_bytes
+        self._check_bytes(records, self.payload_bytes, "records")
         _check(_lib.slc_compress_range(self._h, ctypes.c_int64(chunk_begin), ctypes.c_int64(n_chunks), _dptr(theta),
                                        _dptr(theta_local), _dptr(ef), ctypes.c_float(beta), _dptr(records),
                                        _stream_ptr(stream)), "slc_compress_range")
 
     def index_rank(self, records, ranks, stream=None) -> None:
         """Row f4 (R#28): colex rank of every chunk's index set, ranks: [n_chunks * 16] int32/uint32
-        little-endian limbs."""
-        assert ranks.numel() * ranks.element_size() >= self.n_chunks * 64
+        little-endian limbs.  The first call prepares the plan's binomial table (OPT_INDEX_CODE)."""
+        self._check_bytes(records, self.payload_bytes, "records")
+        self._check_bytes(ranks, self.n_chunks * 64, "ranks")
+        if not self._index_code:
+            self.set_option(OPT_INDEX_CODE, 1)
+            self._index_code = True
         _check(_lib.slc_index_rank(self._h, _dptr(records), _dptr(ranks), _stream_ptr(stream)), "slc_index_rank")
 
     def _peer_args(self, records: Sequence, hdrs, weights):
         R = len(records)
         if not 1 <= R <= MAX_PEERS:
             raise ValueError(f"R={R}")
+        for r in records:
+            self._check_bytes(r, self.payload_bytes, "records")
         ptrs = (ctypes.c_void_p * R)(*[r.data_ptr() for r in records])
         h = None
         if hdrs is not None:
@@ -284,7 +308,9 @@ class Plan:
         """Eq. 2 line 1: agg[shard_elems] f32 <- (1/R) sum_r w_r decode(records[r]).
         weights: host floats; weights_dev: [R] f32 device tensor (e.g. median_norm_weights)."""
         R, ptrs, h, w = self._peer_args(records, hdrs, weights)
+        self._check_f32(agg, "agg")
         if weights_dev is not None:
+            self._check_f32(weights_dev, "weights_dev", R)
             _check(_lib.slc_decode_aggregate_wdev(self._h, h, ptrs, R, _dptr(weights_dev), _dptr(agg),
                                                   _stream_ptr(stream)), "slc_decode_aggregate_wdev")
             return
@@ -302,7 +328,11 @@ class Plan:
         _check(_lib.slc_wire_encode(self._h, _dptr(records), _dptr(wire), _stream_ptr(stream)), "slc_wire_encode")
 
     def wire_decode(self, wire, records, stream=None) -> None:
-        _check(_lib.slc_wire_decode(self._h, _dptr(wire), _dptr(records), _stream_ptr(stream)), "slc_wire_decode")
+        """wire: the shard's body bytes (a shorter buffer -> SlcError(FORMAT_ERROR), nothing read)."""
+        self._check_bytes(records, self.payload_bytes, "records")
+        nbytes = wire.numel() * wire.element_size()
+        _check(_lib.slc_wire_decode(self._h, _dptr(wire), nbytes, _dptr(records), _stream_ptr(stream)),
+               "slc_wire_decode")
 
     # ---- median-norm normalisation (P:101, DESIGN.md R#20)
     def payload_sqnorm(self, records: Sequence, out, hdrs=None, stream=None) -> None:
@@ -320,7 +350,11 @@ class Plan:
     def outer_update(self, theta, alpha: float = 1.0, agg=None, records: Optional[Sequence] = None, hdrs=None,
                      weights=None, stream=None, weights_dev=None) -> None:
         """Eq. 2 line 2: theta <- theta - alpha * Delta; agg=None -> fused decode/aggregate/update."""
+        self._check_dense(theta)
+        if agg is not None:
+            self._check_f32(agg, "agg")
         if weights_dev is not None:
+            self._check_f32(weights_dev, "weights_dev", len(records))
             R, ptrs, h, _ = self._peer_args(records, hdrs, None)
             _check(_lib.slc_outer_update_wdev(self._h, _dptr(theta), h, ptrs, R, _dptr(weights_dev),
                                               ctypes.c_float(alpha), _stream_ptr(stream)), "slc_outer_update_wdev")
@@ -338,10 +372,36 @@ class Plan:
     def check(self) -> None:
         _check(self.get_status(True), "device status")
 
-    def _check_dense(self, *ts):
-        for t in ts:
+    def _check_dense(self, theta, theta_local=None, ef=None):
+        """theta / theta_local in the plan's param dtype, ef fp32; CUDA tensors on the plan's
+        device, contiguous, with at least shard_elems elements."""
+        import torch
+        pdt = torch.bfloat16 if self.dtype == "bf16" else torch.float32
+        for name, t, dt in (("theta", theta, pdt), ("theta_local", theta_local, pdt), ("ef", ef, torch.float32)):
+            if t is None:
+                continue
+            if t.dtype != dt:
+                raise TypeError(f"{name}: dtype {t.dtype}, plan expects {dt}")
+            if not t.is_cuda or t.device.index != self.device:
+                raise ValueError(f"{name}: must be a CUDA tensor on cuda:{self.device}")
+            if not t.is_contiguous():
+                raise ValueError(f"{name}: must be contiguous")
             if t.numel() < self.shard_elems:
-                raise ValueError(f"dense buffer has {t.numel()} < {self.shard_elems} elements")
+                raise ValueError(f"{name}: {t.numel()} < {self.shard_elems} elements")
+
+    def _check_f32(self, t, name, n=None):
+        import torch
+        n = self.shard_elems if n is None else n
+        if t.dtype != torch.float32 or not t.is_cuda or t.device.index != self.device or not t.is_contiguous():
+            raise TypeError(f"{name}: must be a contiguous float32 CUDA tensor on cuda:{self.device}")
+        if t.numel() < n:
+            raise ValueError(f"{name}: {t.numel()} < {n} elements")
+
+    def _check_bytes(self, t, nbytes, name):
+        if t.numel() * t.element_size() < nbytes:
+            raise ValueError(f"{name}: {t.numel() * t.element_size()} < {nbytes} bytes")
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name}: must be a CUDA tensor on cuda:{self.device}")
 
     def close(self):
         if getattr(self, "_h", None):

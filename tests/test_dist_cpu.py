@@ -60,15 +60,18 @@ def _worker(rank, world, port, layout_name, n_peers, q):
                 m[g * gather.slot:g * gather.slot + pg.payload_bytes] = _pattern(pg.info.first_chunk, pg.n_chunks,
                                                                                  rb, r)
             owned.append(m)
-        slices = ex.run(owned)
+        slices = ex.run(owned)           # staged all-to-all
         ok_ex = all(torch.equal(slices[r], _pattern(plan.info.first_chunk, plan.n_chunks, rb, r))
                     for r in range(n_peers))
+        slices = ex.run_p2p(owned)       # grouped send/recv
+        ok_ex &= all(torch.equal(slices[r], _pattern(plan.info.first_chunk, plan.n_chunks, rb, r))
+                     for r in range(n_peers))
         q.put((rank, ok_gather, ok_ex))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,layout_name,n_peers", [(2, "ragged", 5), (3, "llama3.2-1b", 4)])
+@pytest.mark.parametrize("world,layout_name,n_peers", [(2, "ragged", 5), (3, "llama3.2-1b", 4), (3, "ragged", 2)])
 def test_gather_and_exchange_gloo(world, layout_name, n_peers):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

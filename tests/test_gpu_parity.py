@@ -23,20 +23,6 @@ from paper_2603_08163_b200 import slc  # noqa: E402
 DEV = torch.device("cuda:0")
 
 
-# the two decode/update kernels: the persistent pipelined one (default; with a
-# capped grid every CTA walks many chunks) and the one-CTA-per-chunk one
-AGG_KERNELS = {"pipe": {}, "pipe-grid3": {"SLC_AGG_GRID": "3"}, "simple": {"SLC_AGG_KERNEL": "simple"}}
-
-
-@pytest.fixture(params=sorted(AGG_KERNELS))
-def agg_kernel(request, monkeypatch):
-    monkeypatch.delenv("SLC_AGG_KERNEL", raising=False)
-    monkeypatch.delenv("SLC_AGG_GRID", raising=False)
-    for k, v in AGG_KERNELS[request.param].items():
-        monkeypatch.setenv(k, v)
-    return request.param
-
-
 def _compress_gpu(plan, layout, seed, peer, dtype, special_period, warm, theta=None):
     theta, tl, ef = make_device_inputs(plan, layout, seed, peer, dtype, special_period, warm, theta=theta)
     rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device=DEV)
@@ -467,6 +453,10 @@ def test_wire_decode_rejects_invalid_chunks():
         back = torch.zeros_like(rec)
         plan.wire_decode(torch.from_numpy(b).to(DEV), back)
         assert plan.get_status() == slc.INVALID_DATA, name
+    # a truncated body is a format error and nothing is read
+    with pytest.raises(slc.SlcError) as ei:
+        plan.wire_decode(torch.from_numpy(good[:-1]).to(DEV), torch.zeros_like(rec))
+    assert ei.value.status == slc.FORMAT_ERROR
     # untouched bytes decode cleanly again (the latch was cleared by get_status)
     back = torch.zeros_like(rec)
     plan.wire_decode(torch.from_numpy(good).to(DEV), back)

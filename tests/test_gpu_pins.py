@@ -18,17 +18,6 @@ if not torch.cuda.is_available():
 from paper_2603_08163_b200 import slc  # noqa: E402
 
 DEV = torch.device("cuda:0")
-AGG_ENV = {"pipe": {}, "simple": {"SLC_AGG_KERNEL": "simple"}}
-
-
-@pytest.fixture(params=sorted(AGG_ENV))
-def agg_kernel(request, monkeypatch):
-    monkeypatch.delenv("SLC_AGG_KERNEL", raising=False)
-    for k, v in AGG_ENV[request.param].items():
-        monkeypatch.setenv(k, v)
-    return request.param
-
-
 def _expand(ranges, n):
     v = np.zeros(n, np.float32)
     for a, b, x in ranges:

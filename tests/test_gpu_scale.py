@@ -159,11 +159,7 @@ def test_wide_blocked_tensor_takes_warp_kernel(dtype):
 
 @pytest.mark.parametrize("R", [128, 256])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("kern", ["pipe", "simple"])
-def test_crafted_many_peers(R, dtype, kern, monkeypatch):
-    monkeypatch.delenv("SLC_AGG_KERNEL", raising=False)
-    if kern == "simple":
-        monkeypatch.setenv("SLC_AGG_KERNEL", "simple")
+def test_crafted_many_peers(R, dtype, agg_kernel):
     layout = layouts.LAYOUTS["ragged"]
     plan = slc.Plan(layout, dtype=dtype)
     rng = np.random.default_rng(R)
@@ -185,13 +181,9 @@ def test_crafted_many_peers(R, dtype, kern, monkeypatch):
 
 
 @pytest.mark.parametrize("exps,wspan", [((4, 9), 1.0), ((2, 14), 1e4)])
-@pytest.mark.parametrize("kern", ["pipe", "simple"])
-def test_bf16_weighted_fused_update(exps, wspan, kern, monkeypatch):
+def test_bf16_weighted_fused_update(exps, wspan, agg_kernel):
     """bf16 theta + weights (median-norm) through the fused update, both the
     exact fixed-point (narrow) and the sequential fp64 (wide) weighted paths."""
-    monkeypatch.delenv("SLC_AGG_KERNEL", raising=False)
-    if kern == "simple":
-        monkeypatch.setenv("SLC_AGG_KERNEL", "simple")
     layout = layouts.LAYOUTS["ragged"]
     plan = slc.Plan(layout, dtype="bf16")
     rng = np.random.default_rng(900 + exps[1])

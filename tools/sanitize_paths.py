@@ -87,8 +87,8 @@ def main():
         cases += [("1m-2d", "f32", 2, 8), ("1m-1d", "bf16", 2, 32)]
     for c in cases:
         run(*c)
-    if os.environ.get("SLC_AGG_KERNEL") != "simple":
-        os.environ["SLC_AGG_KERNEL"] = "simple"
+    for variant in (2, 3):  # pipelined, one CTA per chunk
+        slc.Plan.default_options = {slc.OPT_AGG_KERNEL: variant}
         run("ragged", "f32", 3, 4)
     print("sanitize_paths done")
 
