@@ -245,6 +245,27 @@ slc_status slc_outer_update_wdev(slc_plan* plan, void* theta_dev, const slc_payl
  *   SLC_ERR_FORMAT on a short buffer, bad magic or version; it fills magic,
  *   version, base_round, peer_id, layout_digest (geometry and chunk range are
  *   not on the wire: the caller's plan supplies them). */
+/* Fast checks on every peer's submission ("fast checks
+ * on all participants (e.g., liveness, synchronization with the main model,
+ * etc.)"; reading R#29).  flags_dev[r] (uint32, device) <- OR of
+ *   SLC_CHECK_LIVENESS  records_dev_host[r] == NULL (no submission this round);
+ *   SLC_CHECK_SYNC      hdrs_host given and hdrs[r].base_round != current_round
+ *                       or hdrs[r].layout_digest != the plan's digest;
+ *   SLC_CHECK_FINITE    a decoded value is non-finite (a used bucket's fp16
+ *                       scale is Inf / NaN), scanned on the device;
+ *   SLC_CHECK_NORM      sqnorm_dev given (slc_payload_sqnorm limbs, summed over
+ *                       the ranks for a sharded job) and the payload norm
+ *                       sqrt(RN64(sum * 2^-48)) > 10 * m, m the lower median of
+ *                       norm_history_host[0..n_hist) (fp64, compared in fp64;
+ *                       n_hist == 0: no norm check).
+ * Unlike slc_decode_aggregate, a peer's header mismatch is reported, not
+ * returned: the round goes on without the flagged peers.  Returns
+ * INVALID_ARGUMENT for R outside [1, 256] or a misaligned flags_dev. */
+enum { SLC_CHECK_LIVENESS = 1, SLC_CHECK_SYNC = 2, SLC_CHECK_FINITE = 4, SLC_CHECK_NORM = 8 };
+slc_status slc_fast_checks(slc_plan* plan, const slc_payload_hdr* hdrs_host, const void* const* records_dev_host,
+                           int32_t R, uint64_t current_round, const uint64_t* sqnorm_dev,
+                           const double* norm_history_host, int32_t n_hist, uint32_t* flags_dev, void* stream);
+
 slc_status slc_wire_layout(const slc_plan* plan, int64_t* body_bytes_host, int64_t* body_offset_host);
 slc_status slc_wire_encode(slc_plan* plan, const void* records_dev, void* wire_dev, void* stream);
 slc_status slc_wire_decode(slc_plan* plan, const void* wire_dev, int64_t nbytes, void* records_dev, void* stream);

@@ -109,7 +109,72 @@ __global__ void __launch_bounds__(kMaxPeers) median_weights_kernel(const unsigne
   }
 }
 
+// fast checks: per peer, flags |= finite (a decoded value is
+// non-finite: a used bucket's scale is Inf / NaN) and norm-sane (the payload
+// norm, from the rank-summed limbs, exceeds `thresh` = 10 x the lower median of
+// the norm history); host-side flags (liveness, sync) come in `hflags`.
+struct FastCheckArgs {
+  uint32_t hflags[kMaxPeers];
+  double thresh;             // +inf: no norm check
+  const unsigned long long* limbs;  // NULL: no norm check
+};
+
+__global__ void __launch_bounds__(256) fast_checks_kernel(const AggArgs a, const FastCheckArgs f, uint32_t* flags) {
+  const int r = blockIdx.y;
+  if (f.hflags[r] & SLC_CHECK_LIVENESS) {  // no submission: nothing to scan
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags + r, f.hflags[r]);
+    return;
+  }
+  const uint32_t* recs = a.rec[r];
+  const int RW = a.g.rec_words, IW = a.g.idx_words, CW = a.g.code_words;
+  bool nonfin = false;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < a.n_chunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int len = __ldg(&a.chunks[c].len);
+    const int k_eff = max(1, (a.g.k * len) / a.g.C);
+    const uint32_t* rec = recs + c * RW;
+    int n_hi = 0;
+    for (int w = 0; w < CW; w++) n_hi += __popc(__ldg(rec + IW + w) & 0xAAAAAAAAu);
+    const uint32_t sw = __ldg(rec + RW - 1);
+    const bool lo_bad = ((sw >> 10) & 0x1Fu) == 0x1Fu, hi_bad = ((sw >> 26) & 0x1Fu) == 0x1Fu;
+    nonfin |= (lo_bad && n_hi < k_eff) || (hi_bad && n_hi > 0);
+  }
+  uint32_t fl = __any_sync(0xFFFFFFFFu, nonfin) ? SLC_CHECK_FINITE : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) fl |= f.hflags[r];
+  if ((threadIdx.x & 31) == 0 && fl) atomicOr(flags + r, fl);
+}
+
+// second launch, one thread per peer: the norm of every finite, present payload
+__global__ void fast_norm_kernel(const FastCheckArgs f, int R, uint32_t* flags) {
+  const int r = threadIdx.x;
+  if (r >= R || !f.limbs || (flags[r] & (SLC_CHECK_LIVENESS | SLC_CHECK_FINITE))) return;
+  u128 v = 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) v += (u128)f.limbs[4 * r + i] << (32 * i);
+  const double x = __dsqrt_rn(__dmul_rn(u128_to_double_rn(v), 0x1p-48));
+  if (x > f.thresh) flags[r] |= SLC_CHECK_NORM;
+}
+
 }  // namespace
+
+cudaError_t launch_fast_checks(const AggArgs& a, const uint32_t* hflags, double thresh,
+                               const unsigned long long* limbs, uint32_t* flags, cudaStream_t s) {
+  FastCheckArgs f;
+  for (int r = 0; r < kMaxPeers; r++) f.hflags[r] = r < a.R ? hflags[r] : 0u;
+  f.thresh = thresh;
+  f.limbs = limbs;
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(uint32_t) * a.R, s);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  const int64_t want = std::max<int64_t>(1, (a.n_chunks + 255) / 256);
+  const int gx = (int)std::min<int64_t>(want, std::max<int64_t>(1, (int64_t)4 * sms / a.R + 1));
+  fast_checks_kernel<<<dim3(gx, a.R), 256, 0, s>>>(a, f, flags);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (limbs) fast_norm_kernel<<<1, kMaxPeers, 0, s>>>(f, a.R, flags);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_payload_sqnorm(const AggArgs& a, unsigned long long* out, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long) * 4 * a.R, s);

@@ -628,6 +628,43 @@ slc_status slc_median_norm_weights(slc_plan* p, int32_t R, const uint64_t* sqnor
                      p);
 }
 
+slc_status slc_fast_checks(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
+                           uint64_t current_round, const uint64_t* sqnorm_dev, const double* hist, int32_t n_hist,
+                           uint32_t* flags_dev, void* stream) {
+  if (!p || p->device < 0 || R < 1 || R > slc::kMaxPeers || !recs || !flags_dev || (((uintptr_t)flags_dev) & 3u))
+    return SLC_ERR_INVALID_ARGUMENT;
+  if (n_hist < 0 || (n_hist > 0 && !hist)) return SLC_ERR_INVALID_ARGUMENT;
+  slc::AggArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.chunks = p->d_chunks;
+  a.n_chunks = p->n_chunks;
+  a.R = R;
+  a.err = p->d_err;
+  a.g = p->g;
+  std::vector<uint32_t> hf(R, 0u);
+  for (int r = 0; r < R; r++) {
+    a.rec[r] = static_cast<const uint32_t*>(recs[r]);
+    if (!recs[r]) {
+      hf[r] |= SLC_CHECK_LIVENESS;
+      continue;
+    }
+    if ((((uintptr_t)recs[r]) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+    if (hdrs && (hdrs[r].base_round != current_round || std::memcmp(hdrs[r].layout_digest, p->digest, 32) != 0))
+      hf[r] |= SLC_CHECK_SYNC;
+  }
+  double thresh = __builtin_inf();
+  if (sqnorm_dev && n_hist > 0) {  // R#29: 10 x the lower median of the history
+    std::vector<double> h(hist, hist + n_hist);
+    std::sort(h.begin(), h.end());
+    thresh = 10.0 * h[(n_hist - 1) / 2];
+  }
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_fast_checks(a, hf.data(), thresh,
+                                             reinterpret_cast<const unsigned long long*>(sqnorm_dev), flags_dev,
+                                             use_stream(p, stream)),
+                     p);
+}
+
 slc_status slc_wire_layout(const slc_plan* p, int64_t* body_bytes, int64_t* body_offset) {
   if (!p || !body_bytes || !body_offset) return SLC_ERR_INVALID_ARGUMENT;
   *body_bytes = p->wire_bytes;

@@ -135,6 +135,9 @@ bool aggregate_batch_supported(const AggArgs& a);
 // median-norm: exact per-peer squared norms as 4 un-carried 32-bit limbs per peer; weights
 cudaError_t launch_payload_sqnorm(const AggArgs& a, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_median_weights(const unsigned long long* limbs, int R, float* w, double* norms, cudaStream_t s);
+// f2 fast checks: finite / norm-sane per peer on the device, host flags ORed in
+cudaError_t launch_fast_checks(const AggArgs& a, const uint32_t* hflags, double thresh,
+                               const unsigned long long* limbs, uint32_t* flags, cudaStream_t s);
 
 #ifdef __CUDACC__
 // weight of canonical peer i (weighted mode)

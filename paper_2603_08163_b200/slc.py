@@ -85,6 +85,7 @@ def _load():
         "slc_wire_header_read": (ctypes.c_int, [P, ctypes.c_int64, pp(PayloadHdr), pp(ctypes.c_int64)]),
         "slc_index_rank": (ctypes.c_int, [P, P, P, P]),
         "slc_plan_set_option": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int64]),
+        "slc_fast_checks": (ctypes.c_int, [P, P, P, ctypes.c_int32, ctypes.c_uint64, P, P, ctypes.c_int32, P, P]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
         "slc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -102,7 +103,11 @@ EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_rec
             "slc_compress", "slc_compress_range", "slc_decode_aggregate", "slc_outer_update", "slc_payload_sqnorm",
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
-            "slc_plan_destroy", "slc_status_string", "slc_index_rank", "slc_plan_set_option"]
+            "slc_plan_destroy", "slc_status_string", "slc_index_rank", "slc_plan_set_option",
+            "slc_fast_checks"]
+
+# slc_fast_checks flag bits (include/slc.h)
+CHECK_LIVENESS, CHECK_SYNC, CHECK_FINITE, CHECK_NORM = 1, 2, 4, 8
 
 # slc_option (include/slc.h)
 OPT_AGG_KERNEL, OPT_AGG_GRID_CAP, OPT_INDEX_CODE = 1, 2, 3
@@ -316,6 +321,24 @@ class Plan:
             return
         _check(_lib.slc_decode_aggregate(self._h, h, ptrs, R, w, _dptr(agg), _stream_ptr(stream)),
                "slc_decode_aggregate")
+
+    def fast_checks(self, records: Sequence, flags, current_round: int = 0, hdrs=None, sqnorm=None,
+                    norm_history=(), stream=None) -> None:
+        """Row f2 fast checks: flags [R] int32 device tensor <- CHECK_* bits per peer.
+        records[r] may be None (no submission: CHECK_LIVENESS); sqnorm: rank-summed [R, 4] limbs."""
+        R = len(records)
+        if not 1 <= R <= MAX_PEERS:
+            raise ValueError(f"R={R}")
+        for r in records:
+            if r is not None:
+                self._check_bytes(r, self.payload_bytes, "records")
+        ptrs = (ctypes.c_void_p * R)(*[0 if r is None else r.data_ptr() for r in records])
+        h = None if hdrs is None else (PayloadHdr * R)(*hdrs)
+        hist = [float(x) for x in norm_history]
+        harr = (ctypes.c_double * max(1, len(hist)))(*hist) if hist else None
+        assert flags.numel() >= R and flags.element_size() == 4
+        _check(_lib.slc_fast_checks(self._h, h, ptrs, R, ctypes.c_uint64(current_round), _dptr(sqnorm), harr,
+                                    len(hist), _dptr(flags), _stream_ptr(stream)), "slc_fast_checks")
 
     # ---- SLC1 wire format (NEXT row f2, SPEC S:137-145)
     def wire_layout(self):
