@@ -366,7 +366,7 @@ def run_slc(args):
         "clocks": clk.summary(),
     }
     if args.index_code:
-        out["index_code"] = time_index_rank(plan, shard, stream)
+        out["index_code"] = time_index_rank(plan, shard, stream, R, recs)
     if offload is not None:
         out["config"]["ef_offload"] = {"mode": args.ef_offload, "pieces": len(offload.pieces),
                                        **time_offload(offload, stream, reps=3)}
@@ -389,22 +389,47 @@ def run_slc(args):
     return out if rank == 0 else None
 
 
-def time_index_rank(plan, shard, stream, reps=5):
-    """Row f4: slc_index_rank over the shard's own records (not in the timed step)."""
+def time_index_rank(plan, shard, stream, R, recs, reps=5):
+    """Row f4 (not in the timed step): the colex rank alone, the entropy-coded
+    record encode / decode (GPU unrank) of one payload, and the update fed by
+    entropy-coded payloads (R decodes + the fused update) against the update
+    on fixed-width records."""
     import torch
-    ranks = torch.empty(plan.n_chunks * 16, dtype=torch.int32, device=shard.records.device)
-    plan.index_rank(shard.records, ranks, stream=stream)  # builds the binomial table once
+    dev = shard.records.device
+    ranks = torch.empty(plan.n_chunks * 16, dtype=torch.int32, device=dev)
+    ec = torch.empty(plan.n_chunks * plan.ec_record_bytes, dtype=torch.uint8, device=dev)
+    tmp = [torch.empty(plan.payload_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+    plan.index_rank(shard.records, ranks, stream=stream)  # prepares the binomial table once
+    plan.index_encode(shard.records, ec, stream=stream)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(reps):
-        plan.index_rank(shard.records, ranks, stream=stream)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
-    return {"ms": ms, "chunks": plan.n_chunks, "chunks_per_s": plan.n_chunks / (ms * 1e-3),
-            "bits_per_chunk_full": 472, "note": "R#28 colex rank; reads the 96-B index field + 64 binomial "
-            "table rows (15.7 MB table, L2-resident) per chunk, writes 64 B"}
+
+    def timed(fn, n=reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    rank_ms = timed(lambda: plan.index_rank(shard.records, ranks, stream=stream))
+    enc_ms = timed(lambda: plan.index_encode(shard.records, ec, stream=stream))
+    dec_ms = timed(lambda: plan.index_decode(ec, tmp[0], stream=stream))
+    th = shard.theta.clone()
+    upd_ms = timed(lambda: plan.outer_update(th, ALPHA, records=recs, stream=stream), 3)
+    if plan.get_status() != 0:
+        raise RuntimeError("index code: device status")
+    del th
+    return {"rank_ms": rank_ms, "encode_ms": enc_ms, "decode_ms": dec_ms, "chunks": plan.n_chunks,
+            "record_bytes": plan.record_bytes, "ec_record_bytes": plan.ec_record_bytes,
+            "payload_bytes": plan.payload_bytes, "ec_payload_bytes": plan.n_chunks * plan.ec_record_bytes,
+            "update_fixed_width_ms": upd_ms, "update_from_ec_ms": R * dec_ms + upd_ms, "R": R,
+            "note": "R#28: 15 rank limbs + codes + scales per chunk (80 B vs 116 B); decode = greedy colex "
+                    "unranking, a 32-way warp search per position; update_from_ec = R decodes + the fused update "
+                    "(the record bytes the update reads drop 31 %, the unranking costs far more: P:91-93's "
+                    "'significant overhead')"}
 
 
 def time_offload(offload, stream, reps=3):

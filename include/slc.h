@@ -285,6 +285,25 @@ slc_status slc_wire_header_read(const uint8_t* in_host, int64_t nbytes, slc_payl
  * buffers; INVALID_ARGUMENT otherwise. */
 slc_status slc_index_rank(slc_plan* plan, const void* records_dev, uint32_t* ranks_dev, void* stream);
 
+/* Entropy-coded ("EC") records (row f4, reading R#28): the 12-bit index stream
+ * of each record replaced by its colex rank.  EC record of chunk c at byte
+ * c*ec_record_bytes, little-endian u32 words: 0..14 the rank (limb 0 least
+ * significant; < binom(C_eff, k_eff) < 2^472), then the record's code words
+ * (R#6: bit 2j sign, 2j+1 bucket of slot j) and its scale word (S_lo | S_hi<<16).
+ * 80 bytes at C = 4096, k = 64 against 116 (ratio 16384/80 = 204.8x dense fp32).
+ * slc_ec_record_bytes: that size; -1 off the paper geometry (C = 4096, k <= 64,
+ *   12-bit indices).
+ * slc_index_encode: records_dev (slc_compress layout) -> ec_dev.
+ * slc_index_decode: ec_dev -> records_dev (R#6 layout, unused slots zero) by
+ *   greedy colex unranking (p_i = the largest p with binom(p, i+1) <= the
+ *   remaining rank, i = k_eff-1 .. 0); a rank that is not a valid code
+ *   (>= binom(C_eff, k_eff)) latches INVALID_DATA.
+ * Both need the plan's binomial table (SLC_OPT_INDEX_CODE); UNSUPPORTED off the
+ * paper geometry; 4-byte aligned buffers. */
+int64_t slc_ec_record_bytes(const slc_geometry* geom_host);
+slc_status slc_index_encode(slc_plan* plan, const void* records_dev, void* ec_dev, void* stream);
+slc_status slc_index_decode(slc_plan* plan, const void* ec_dev, void* records_dev, void* stream);
+
 /* Plan options (configuration calls: synchronous, may allocate).
  *  SLC_OPT_AGG_KERNEL    which decode / fused-update implementation runs:
  *                        0 auto (default: the persistent pipelined kernel

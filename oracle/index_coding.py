@@ -77,3 +77,52 @@ def decode(bits: str, C: int, k: int) -> List[int]:
 def bits_per_value(C: int, k: int) -> float:
     """Realised index cost of the code, bits per transmitted value."""
     return code_bits(C, k) / k
+
+
+# ---------------------------------------------------------------- entropy-coded device records (R#28)
+# An entropy-coded ("EC") record replaces the 12-bit index stream of a device
+# record (R#6) with the chunk's colex rank: 15 little-endian 32-bit limbs
+# (rank < binom(C_eff, k_eff) <= binom(4096, 64) < 2^472, so the top 8 of the
+# 480 bits are zero), followed by the record's code words (bit 2j = sign,
+# 2j+1 = bucket of slot j, as R#6) and its scale word: 15 + ceil(2k/32) + 1
+# words = 80 bytes at k = 64 (116 for the fixed-width record).
+EC_RANK_LIMBS = 15
+
+
+def ec_record_words(k: int = 64) -> int:
+    return EC_RANK_LIMBS + (2 * k + 31) // 32 + 1
+
+
+def ec_from_record(rec_words, n: int, k: int = 64, ib: int = 12):
+    """EC record (list of uint32) of a fixed-width record (R#6 words) of a chunk
+    of n positions: decode the ascending positions with the C oracle, rank them
+    (plain definition), copy the code and scale words."""
+    from . import decode_chunk, geom as _geom
+    import numpy as np
+    g = _geom(k=k, index_bits=ib)
+    rec = np.asarray(rec_words, np.uint32)
+    pos, _ = decode_chunk(rec, n, g)
+    r = rank([int(p) for p in pos], n)
+    assert r < 1 << (32 * EC_RANK_LIMBS)
+    iw = (k * ib + 31) // 32
+    cw = (2 * k + 31) // 32
+    limbs = [(r >> (32 * i)) & 0xFFFFFFFF for i in range(EC_RANK_LIMBS)]
+    return limbs + [int(w) for w in rec[iw:iw + cw]] + [int(rec[iw + cw])]
+
+
+def record_from_ec(ec_words, n: int, k_eff: int, k: int = 64, ib: int = 12):
+    """Inverse: the fixed-width record (R#6 layout, unused slots zero) of an EC record."""
+    ec = [int(w) for w in ec_words]
+    r = sum(ec[i] << (32 * i) for i in range(EC_RANK_LIMBS))
+    pos = unrank(r, n, k_eff)
+    iw = (k * ib + 31) // 32
+    cw = (2 * k + 31) // 32
+    words = [0] * (iw + cw + 1)
+    for j, p in enumerate(pos):
+        b = ib * j
+        for bit in range(ib):
+            if (p >> bit) & 1:
+                words[(b + bit) // 32] |= 1 << ((b + bit) % 32)
+    words[iw:iw + cw] = ec[EC_RANK_LIMBS:EC_RANK_LIMBS + cw]
+    words[iw + cw] = ec[EC_RANK_LIMBS + cw]
+    return words

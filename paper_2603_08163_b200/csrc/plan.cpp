@@ -719,6 +719,38 @@ slc_status slc_index_rank(slc_plan* p, const void* records, uint32_t* ranks, voi
                      p);
 }
 
+int64_t slc_ec_record_bytes(const slc_geometry* geom) {
+  if (check_geom(geom) != SLC_OK) return -1;
+  const slc::Geom g = make_geom(*geom);
+  if (!slc::index_rank_supported(g)) return -1;
+  return 4 * (int64_t)slc::ec_record_words(g);
+}
+
+slc_status slc_index_encode(slc_plan* p, const void* records, void* ec, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (!slc::index_rank_supported(p->g)) return SLC_ERR_UNSUPPORTED;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!p->d_binom) return SLC_ERR_INVALID_ARGUMENT;  // slc_plan_set_option(SLC_OPT_INDEX_CODE, 1) first
+  if (!records || !ec || (((uintptr_t)records) & 3u) || (((uintptr_t)ec) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_index_encode(p->d_chunks, p->n_chunks, static_cast<const uint32_t*>(records),
+                                              p->d_binom, static_cast<uint32_t*>(ec), p->g, use_stream(p, stream)),
+                     p);
+}
+
+slc_status slc_index_decode(slc_plan* p, const void* ec, void* records, void* stream) {
+  if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
+  if (!slc::index_rank_supported(p->g)) return SLC_ERR_UNSUPPORTED;
+  if (p->n_chunks == 0) return SLC_OK;
+  if (!p->d_binom) return SLC_ERR_INVALID_ARGUMENT;
+  if (!records || !ec || (((uintptr_t)records) & 3u) || (((uintptr_t)ec) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_index_decode(p->d_chunks, p->n_chunks, static_cast<const uint32_t*>(ec),
+                                              p->d_binom, static_cast<uint32_t*>(records), p->d_err, p->g,
+                                              use_stream(p, stream)),
+                     p);
+}
+
 slc_status slc_plan_set_option(slc_plan* p, int32_t option, int64_t value) {
   if (!p) return SLC_ERR_INVALID_ARGUMENT;
   switch (option) {

@@ -113,6 +113,12 @@ size_t binom_table_bytes(const Geom& g);
 cudaError_t build_binom_table(uint32_t* T, const Geom& g, cudaStream_t s);
 cudaError_t launch_index_rank(const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* rec, const uint32_t* T,
                               uint32_t* ranks, const Geom& g, cudaStream_t s);
+// entropy-coded records (R#28): rank limbs + code words + scale word
+int ec_record_words(const Geom& g);
+cudaError_t launch_index_encode(const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* rec, const uint32_t* T,
+                                uint32_t* ec, const Geom& g, cudaStream_t s);
+cudaError_t launch_index_decode(const ChunkDesc* chunks, int64_t n_chunks, const uint32_t* ec, const uint32_t* T,
+                                uint32_t* rec, uint32_t* err, const Geom& g, cudaStream_t s);
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);

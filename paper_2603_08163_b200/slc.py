@@ -85,6 +85,9 @@ def _load():
         "slc_wire_header_read": (ctypes.c_int, [P, ctypes.c_int64, pp(PayloadHdr), pp(ctypes.c_int64)]),
         "slc_index_rank": (ctypes.c_int, [P, P, P, P]),
         "slc_plan_set_option": (ctypes.c_int, [P, ctypes.c_int32, ctypes.c_int64]),
+        "slc_ec_record_bytes": (ctypes.c_int64, [pp(Geometry)]),
+        "slc_index_encode": (ctypes.c_int, [P, P, P, P]),
+        "slc_index_decode": (ctypes.c_int, [P, P, P, P]),
         "slc_fast_checks": (ctypes.c_int, [P, P, P, ctypes.c_int32, ctypes.c_uint64, P, P, ctypes.c_int32, P, P]),
         "slc_get_status": (ctypes.c_int, [P, ctypes.c_int32]),
         "slc_plan_destroy": (None, [P]),
@@ -104,7 +107,7 @@ EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_rec
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
             "slc_plan_destroy", "slc_status_string", "slc_index_rank", "slc_plan_set_option",
-            "slc_fast_checks"]
+            "slc_fast_checks", "slc_ec_record_bytes", "slc_index_encode", "slc_index_decode"]
 
 # slc_fast_checks flag bits (include/slc.h)
 CHECK_LIVENESS, CHECK_SYNC, CHECK_FINITE, CHECK_NORM = 1, 2, 4, 8
@@ -288,10 +291,31 @@ class Plan:
         little-endian limbs.  The first call prepares the plan's binomial table (OPT_INDEX_CODE)."""
         self._check_bytes(records, self.payload_bytes, "records")
         self._check_bytes(ranks, self.n_chunks * 64, "ranks")
+        self._prepare_index_code()
+        _check(_lib.slc_index_rank(self._h, _dptr(records), _dptr(ranks), _stream_ptr(stream)), "slc_index_rank")
+
+    @property
+    def ec_record_bytes(self) -> int:
+        return int(_lib.slc_ec_record_bytes(ctypes.byref(self.geom)))
+
+    def _prepare_index_code(self):
         if not self._index_code:
             self.set_option(OPT_INDEX_CODE, 1)
             self._index_code = True
-        _check(_lib.slc_index_rank(self._h, _dptr(records), _dptr(ranks), _stream_ptr(stream)), "slc_index_rank")
+
+    def index_encode(self, records, ec, stream=None) -> None:
+        """Row f4 (R#28): fixed-width records -> entropy-coded records (n_chunks * ec_record_bytes)."""
+        self._check_bytes(records, self.payload_bytes, "records")
+        self._check_bytes(ec, self.n_chunks * self.ec_record_bytes, "ec")
+        self._prepare_index_code()
+        _check(_lib.slc_index_encode(self._h, _dptr(records), _dptr(ec), _stream_ptr(stream)), "slc_index_encode")
+
+    def index_decode(self, ec, records, stream=None) -> None:
+        """Row f4 (R#28): entropy-coded records -> fixed-width records (greedy colex unranking on the GPU)."""
+        self._check_bytes(ec, self.n_chunks * self.ec_record_bytes, "ec")
+        self._check_bytes(records, self.payload_bytes, "records")
+        self._prepare_index_code()
+        _check(_lib.slc_index_decode(self._h, _dptr(ec), _dptr(records), _stream_ptr(stream)), "slc_index_decode")
 
     def _peer_args(self, records: Sequence, hdrs, weights):
         R = len(records)

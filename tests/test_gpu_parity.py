@@ -562,3 +562,37 @@ def test_index_rank_unsupported_geometry():
     ranks = torch.zeros(plan.n_chunks * 16, dtype=torch.int32, device=DEV)
     with pytest.raises(slc.SlcError):
         plan.index_rank(rec, ranks)
+
+
+@pytest.mark.parametrize("name", ["ragged", "1m-2d", "1m-1d"])
+@pytest.mark.parametrize("special", [0, 4])
+def test_index_ec_encode_decode_parity(name, special):
+    """Row f4 (R#28): GPU entropy-coded records equal the oracle's EC records word
+    for word; the GPU unrank (slc_index_decode) gives back the fixed-width records
+    bit for bit, from the GPU's and from the oracle's EC records."""
+    from oracle import index_coding as ic
+    from helpers import shard_chunk_lengths
+    layout = layouts.LAYOUTS[name]
+    plan = slc.Plan(layout, dtype="f32")
+    ref_rec, _, _ = oracle_compress_shard(plan, layout, 13, 2, "f32", special, special == 0)
+    rec = torch.from_numpy(ref_rec.view(np.uint8).copy()).to(DEV)
+    assert plan.ec_record_bytes == 80
+    ec = torch.zeros(plan.n_chunks * plan.ec_record_bytes, dtype=torch.uint8, device=DEV)
+    plan.index_encode(rec, ec)
+    RW = ref_rec.size // plan.n_chunks
+    lens = shard_chunk_lengths(plan)
+    want = np.array([ic.ec_from_record(ref_rec[c * RW:(c + 1) * RW], n) for c, n in enumerate(lens)], np.uint32)
+    got = ec.cpu().numpy().view(np.uint32).reshape(plan.n_chunks, -1)
+    assert np.array_equal(got, want)
+    back = torch.zeros_like(rec)
+    plan.index_decode(ec, back)
+    assert plan.get_status() == slc.OK
+    assert torch.equal(back, rec)
+    back2 = torch.zeros_like(rec)
+    plan.index_decode(torch.from_numpy(want.view(np.uint8).copy().reshape(-1)).to(DEV), back2)
+    assert plan.get_status() == slc.OK and torch.equal(back2, rec)
+    # a rank beyond binom(C_eff, k_eff) is not a code: INVALID_DATA
+    bad = want.copy()
+    bad[0, 14] = 0x00FFFFFF
+    plan.index_decode(torch.from_numpy(bad.view(np.uint8).copy().reshape(-1)).to(DEV), back2)
+    assert plan.get_status() == slc.INVALID_DATA

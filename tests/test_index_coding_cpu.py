@@ -55,3 +55,23 @@ def test_extremes():
         ic.rank([5, C], C)
     with pytest.raises(ValueError):
         ic.decode("0" * 471, C, k)
+
+
+def test_ec_record_round_trip_against_the_fixed_width_record():
+    """EC record (R#28): rank limbs + code words + scale word; 80 B at k = 64; the
+    inverse reproduces the R#6 record exactly (test-side packer as the reference)."""
+    import numpy as np
+    import oracle
+    from helpers import pack_record
+    assert ic.ec_record_words(64) * 4 == 80
+    rng = np.random.default_rng(4)
+    for n in [4096, 2048, 100, 1]:
+        ke = oracle.effective_k(n)
+        for _ in range(10):
+            pos = np.sort(rng.choice(n, ke, replace=False))
+            codes = rng.integers(0, 4, ke)
+            rec = pack_record(pos, codes, 0x3C00, 0x4000, 64, 12)
+            ec = ic.ec_from_record(rec, n)
+            assert len(ec) == 20 and ec[14] >> 24 == 0
+            assert sum(ec[i] << (32 * i) for i in range(15)) == ic.rank(pos.tolist(), n)
+            assert ic.record_from_ec(ec, n, ke) == [int(w) for w in rec]
