@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--index-code", action="store_true",
                     help="row f4: also time slc_index_rank (colex index code, R#28) on the step's records")
     ap.add_argument("--ef-pieces", type=int, default=16, help="pieces of the pipelined EF swap (row f3)")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1, row a8: p2p = records pushed into every rank's message over NVLink peer memory by "
+                         "the compress kernel (slc_compress_multi + device barrier); nccl = all_gather_into_tensor")
     ap.add_argument("--agg-kernel", default="auto", choices=["auto", "batch", "pipe", "simple"],
                     help="decode / fused-update implementation (SLC_OPT_AGG_KERNEL; auto = batched where it applies)")
     return ap.parse_args()
@@ -218,6 +221,10 @@ def run_slc(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # more NCCL channels / larger P2P chunks: measured 1.3-1.5x on the a8 all-gather and the a9
+        # all-to-all at these message sizes on B200 (tools/coll_bench.py, profiles/r02_collectives.txt)
+        os.environ.setdefault("NCCL_MIN_NCHANNELS", "64")
+        os.environ.setdefault("NCCL_P2P_NET_CHUNKSIZE", "524288")
         dist.init_process_group("nccl", device_id=dev)
     wl = args.workload or ("llama3.2-1b" if world == 1 else "llama3-8b")
     lname, R, dtype = WORKLOADS[wl]
@@ -231,9 +238,13 @@ def run_slc(args):
     else:
         plan = slc.Plan(layout, geom=slc.geometry(args.block, args.k), rank=rank, nranks=world, dtype=dtype,
                         device=local)
-    gather = sdist.PayloadGather(plan) if world > 1 else None
-    shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=True,
-                       records=gather.alloc_records() if gather else None)
+    gather = pmsg = None
+    if world > 1:
+        if args.gather == "p2p":
+            pmsg = sdist.PeerMessage(plan)
+        gather = sdist.PayloadGather(plan)  # also the a8 reference timing in `collectives`
+    own_records = pmsg.records if pmsg is not None else (gather.alloc_records() if gather else None)
+    shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=True, records=own_records)
     peers = make_peer_records(plan, layout, shard, seed=0, n_peers=R - 1, first_peer=1, dtype=dtype)
     shard.reset()
     recs = [shard.records[:plan.payload_bytes]] + peers
@@ -257,20 +268,24 @@ def run_slc(args):
             ev[i][0].record(stream)
         if pipelined:  # compress_ms then includes the exposed part of the swaps
             offload.compress_pipelined(shard.theta, shard.theta_local, shard.records, beta=BETA, stream=stream)
+        elif pmsg is not None:  # a8 folded into compress: records pushed to every rank's message
+            pmsg.compress(shard.theta, shard.theta_local, ef, beta=BETA, stream=stream)
         else:
             plan.compress(shard.theta, shard.theta_local, ef, shard.records, beta=BETA, stream=stream)
         if i is not None:
             ev[i][1].record(stream)
         if offload is not None and not pipelined:
             offload.swap_out(stream)
-        if gather is not None:
+        if gather is not None and pmsg is None:
             gather.start(shard.records)
         if mnorm is not None:
             w = mnorm(recs, hdrs=hdrs, stream=stream)
             plan.outer_update(shard.theta, ALPHA, records=recs, hdrs=hdrs, weights_dev=w, stream=stream)
         else:
             plan.outer_update(shard.theta, ALPHA, records=recs, stream=stream)
-        if gather is not None:
+        if pmsg is not None:
+            pmsg.wait(stream)  # every rank's shard is in every rank's message
+        elif gather is not None:
             gather.wait()
         if offload is not None:
             offload.wait(stream)
@@ -309,7 +324,12 @@ def run_slc(args):
 
     extra = {}
     if world > 1:
-        extra = time_collectives(plan, gather, shard, R, stream, dev)
+        rec_for_gather = gather.alloc_records()
+        rec_for_gather[:plan.payload_bytes].copy_(shard.records[:plan.payload_bytes])
+        extra = time_collectives(plan, gather, rec_for_gather, R, stream, dev, pmsg=pmsg)
+        extra["a8_in_step"] = ("p2p: slc_compress_multi pushes each record into every rank's peer message over NVLink "
+                               "(symmetric memory) + a device barrier; no collective" if pmsg is not None else
+                               "nccl: all_gather_into_tensor overlapped with the fused update")
 
     info = plan.info
     P_total = info.total_elems
@@ -349,7 +369,7 @@ def run_slc(args):
         "config": {"workload": f"{wl} ({P_total} params), R={R} peers, C={args.block ** 2} k={args.k} 2-bit, "
                                f"beta={BETA} alpha={ALPHA}",
                    "params": P_total, "peers": R, "parallelism": f"fsdp-shard{world}",
-                   "agg_kernel": args.agg_kernel,
+                   "agg_kernel": args.agg_kernel, **({"gather": args.gather} if world > 1 else {}),
                    "l2": "inputs > L2 (126 MB): no flush needed"},
         "hbm_gbs": step_gbs_rank * world,
         "hbm_frac_of_peak": step_gbs_rank / peak,
@@ -457,7 +477,7 @@ def time_offload(offload, stream, reps=3):
     return res
 
 
-def time_collectives(plan, gather, shard, R, stream, dev, reps=5):
+def time_collectives(plan, gather, records, R, stream, dev, reps=5, pmsg=None):
     """a8 all-gather of the shard payloads alone, and the a9 simulated-peer
     exchange (peer r's full message on rank r % n; each rank receives its slice
     of every message) — both max over ranks, reported beside the step."""
@@ -467,13 +487,13 @@ def time_collectives(plan, gather, shard, R, stream, dev, reps=5):
     world, rank = dist.get_world_size(), dist.get_rank()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    gather.start(shard.records)
+    gather.start(records)
     gather.wait()
     torch.cuda.synchronize()
     dist.barrier()
     a.record(stream)
     for _ in range(reps):
-        gather.start(shard.records)
+        gather.start(records)
         gather.wait()
     b.record(stream)
     torch.cuda.synchronize()
@@ -497,17 +517,40 @@ def time_collectives(plan, gather, shard, R, stream, dev, reps=5):
     ex_ms = timed(ex.exchange)
     p2p_ms = timed(lambda: ex.run_p2p(owned))
     del ex
-    t = torch.tensor([ag_ms, ex_ms, p2p_ms], dtype=torch.float64, device=dev)
+    exp = sdist.PeerExchangeP2P(plan, gather.sizes, gather.slot, R)
+    for i, m in enumerate(owned):
+        exp.stage(i, m)
+    pull_ms = timed(lambda: exp.exchange(stream))
+    del exp
+    agp_ms = 0.0
+    if pmsg is not None:  # a8 data movement alone over NVLink: pull every other rank's slot
+        local = torch.empty(world * pmsg.slot, dtype=torch.uint8, device=dev)
+        base = [int(pmsg.handle.buffer_ptrs[g]) for g in range(world)]
+        pairs = [(base[g] + g * pmsg.slot, local.data_ptr() + g * pmsg.slot, pmsg.sizes[g])
+                 for g in range(world) if g != rank]
+
+        def pull():
+            pmsg.handle.barrier(channel=0)
+            plan.peer_copy(pairs, stream=stream)
+
+        agp_ms = timed(pull)
+        del local
+    t = torch.tensor([ag_ms, ex_ms, p2p_ms, pull_ms, agp_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ag_ms, ex_ms, p2p_ms = t.tolist()
+    ag_ms, ex_ms, p2p_ms, pull_ms, agp_ms = t.tolist()
     moved = R * plan.payload_bytes * (world - 1) / world  # bytes per rank that cross NVLink
     msg = sum(gather.sizes)
     return {"allgather_ms": ag_ms, "allgather_message_bytes": msg,
             "allgather_busbw_gbs": msg * (world - 1) / world / (ag_ms * 1e-3) / 1e9,
+            **({"allgather_pull_ms": agp_ms,
+                "allgather_pull_busbw_gbs": msg * (world - 1) / world / (agp_ms * 1e-3) / 1e9} if agp_ms else {}),
             "exchange_ms": ex_ms, "exchange_bytes_per_rank": R * plan.payload_bytes,
             "exchange_gbs_per_rank": moved / (ex_ms * 1e-3) / 1e9,
-            "exchange_p2p_ms": p2p_ms, "exchange_method": "staged all_to_all_single (one NCCL call); "
-                                                          "p2p = grouped send/recv per (peer, dst) slice",
+            "exchange_p2p_ms": p2p_ms, "exchange_pull_ms": pull_ms,
+            "exchange_pull_gbs_per_rank": moved / (pull_ms * 1e-3) / 1e9,
+            "exchange_method": "staged all_to_all_single (one NCCL call); p2p = grouped send/recv per (peer, dst) "
+                               "slice; pull = every rank pulls its slices from the owners' symmetric-memory "
+                               "messages over NVLink with one slc_peer_copy kernel between two device barriers",
             "note": "all-gather overlapped with the fused update inside the step; exchange (stand-in for the "
                     "R2 download) reported separately, not in ms_per_step"}
 

@@ -150,6 +150,29 @@ slc_status slc_layout_digest(const slc_geometry* geom_host, const slc_tensor* la
 slc_status slc_compress(slc_plan* plan, const void* theta_dev, const void* theta_local_dev, float* ef_dev,
                         float beta, void* records_dev, void* stream);
 
+/* slc_compress that writes the shard's records to n_out buffers at once:
+ * records_out_host[0] (the caller's own, as records_dev of slc_compress) and
+ * records_out_host[1..n_out-1], device pointers valid on the plan's device —
+ * typically NVLink peer mappings of every other rank's peer-message buffer at
+ * this shard's offset (CUDA IPC / symmetric memory), so the intra-box payload
+ * all-gather of row a8 is folded into the compress
+ * kernel: each 116-B record is stored to every destination as it is packed,
+ * and no separate collective runs.  The caller synchronises the ranks after
+ * the call (e.g. a device-side barrier) before reading a gathered message.
+ * 1 <= n_out <= 16; 4-byte aligned destinations. */
+slc_status slc_compress_multi(slc_plan* plan, const void* theta_dev, const void* theta_local_dev, float* ef_dev,
+                              float beta, void* const* records_out_host, int32_t n_out, void* stream);
+
+/* Rows a8 / a9 over NVLink peer memory: copy n byte ranges (src_host[i] ->
+ * dst_host[i], bytes_host[i] bytes; device pointers valid on the plan's device,
+ * either side may be a peer mapping of another GPU's buffer) with one kernel
+ * in which every SM pulls 32 KB at a time, so all links stream at once — the
+ * simulated-peer exchange pulls each rank's slice of every peer message from
+ * its owner this way.  16-B aligned ranges take the vector path.  The caller
+ * orders it against the peers (device barrier).  0 <= n <= 256. */
+slc_status slc_peer_copy(slc_plan* plan, const void* const* src_host, void* const* dst_host,
+                         const int64_t* bytes_host, int32_t n, void* stream);
+
 /* slc_compress restricted to the shard-local chunks [chunk_begin, chunk_begin + n_chunks)
  * (same buffers and meaning as slc_compress: full-shard theta / theta_local / ef
  * base pointers, records_dev the full shard record buffer, chunk c at byte

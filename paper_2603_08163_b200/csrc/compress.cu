@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(C / 16) compress_kernel(const CompressArgs a) 
     }
     __syncwarp();
     const QuantOut qo = warp_quantize_pack(selpos, selval, selcode, k, k_eff, a.g,
-                                           a.records + chunk * a.g.rec_words, a.err);
+                                           a.records + chunk * a.g.rec_words, a.err, a.rec_extra, a.n_extra,
+                                           chunk * a.g.rec_words);
     if (lane == 0) { s_tau = qo.tau; s_flo = qo.flo; s_fhi = qo.fhi; }
   }
   __syncthreads();

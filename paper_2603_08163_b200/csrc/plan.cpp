@@ -46,6 +46,10 @@ struct slc_plan {
   int64_t wire_bytes = 0, wire_offset = 0;
   // f4 index code: binomial table binom(p, j), built by slc_plan_set_option(SLC_OPT_INDEX_CODE)
   uint32_t* d_binom = nullptr;
+  // slc_compress_multi: device array of the extra record destinations
+  uint64_t* d_rec_extra = nullptr;
+  int n_extra_next = 0;
+  void* d_pc_scratch = nullptr;  // slc_peer_copy's segment table
   // slc_plan_set_option
   int agg_variant = 0;
   int64_t agg_grid_cap = 0;
@@ -451,11 +455,15 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     if (ce == cudaSuccess)
       ce = cudaMemcpy(p->d_chunks, table.data(), table.size() * sizeof(ChunkDesc), cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_wire_off, wire_off.size() * sizeof(int64_t));
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_rec_extra, slc::kMaxRecOut * sizeof(uint64_t));
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_pc_scratch, slc::peer_copy_scratch_bytes());
     if (ce == cudaSuccess)
       ce = cudaMemcpy(p->d_wire_off, wire_off.data(), wire_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
   }
   if (ce != cudaSuccess) {
     if (p->d_wire_off) cudaFree(p->d_wire_off);
+    if (p->d_rec_extra) cudaFree(p->d_rec_extra);
+    if (p->d_pc_scratch) cudaFree(p->d_pc_scratch);
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
@@ -495,6 +503,27 @@ slc_status slc_compress(slc_plan* p, const void* theta, const void* theta_local,
   return slc_compress_range(p, 0, p->n_chunks, theta, theta_local, ef, beta, records, stream);
 }
 
+slc_status slc_compress_multi(slc_plan* p, const void* theta, const void* theta_local, float* ef, float beta,
+                              void* const* records_out, int32_t n_out, void* stream) {
+  if (!p || p->device < 0 || !records_out || n_out < 1 || n_out > slc::kMaxRecOut) return SLC_ERR_INVALID_ARGUMENT;
+  uint64_t h[slc::kMaxRecOut];
+  for (int i = 1; i < n_out; i++) {
+    if (!records_out[i] || (((uintptr_t)records_out[i]) & 3u)) return SLC_ERR_INVALID_ARGUMENT;
+    h[i - 1] = (uint64_t)(uintptr_t)records_out[i];
+  }
+  if (n_out > 1 && p->n_chunks > 0) {
+    DeviceGuard guard(p->device);
+    // stream-ordered: the kernel below reads the pointers after this copy
+    cudaError_t e = cudaMemcpyAsync(p->d_rec_extra, h, sizeof(uint64_t) * (n_out - 1), cudaMemcpyHostToDevice,
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_status(e, p);
+  }
+  p->n_extra_next = n_out - 1;
+  const slc_status st = slc_compress_range(p, 0, p->n_chunks, theta, theta_local, ef, beta, records_out[0], stream);
+  p->n_extra_next = 0;
+  return st;
+}
+
 slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* theta, const void* theta_local,
                               float* ef, float beta, void* records, void* stream) {
   if (!p || p->device < 0) return SLC_ERR_INVALID_ARGUMENT;
@@ -517,6 +546,8 @@ slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* t
   a.beta = beta;
   a.max_ld = p->max_ld;
   a.g = p->g;
+  a.rec_extra = p->d_rec_extra;
+  a.n_extra = p->n_extra_next;
   DeviceGuard guard(p->device);
   cudaStream_t st = use_stream(p, stream);
   if (slc::compress_tma_supported(p->g)) {
@@ -626,6 +657,17 @@ slc_status slc_median_norm_weights(slc_plan* p, int32_t R, const uint64_t* sqnor
   return cuda_status(slc::launch_median_weights(reinterpret_cast<const unsigned long long*>(sqnorm_dev), R,
                                                 weights_dev, norms_dev, use_stream(p, stream)),
                      p);
+}
+
+slc_status slc_peer_copy(slc_plan* p, const void* const* src, void* const* dst, const int64_t* bytes, int32_t n,
+                         void* stream) {
+  if (!p || p->device < 0 || n < 0 || n > slc::kMaxPeers || (n > 0 && (!src || !dst || !bytes)))
+    return SLC_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; i++)
+    if (bytes[i] < 0 || (bytes[i] > 0 && (!src[i] || !dst[i]))) return SLC_ERR_INVALID_ARGUMENT;
+  if (!p->d_pc_scratch) return SLC_OK;  // plan without device tables: nothing to copy into (n_chunks == 0)
+  DeviceGuard guard(p->device);
+  return cuda_status(slc::launch_peer_copy(src, dst, bytes, n, p->d_pc_scratch, use_stream(p, stream)), p);
 }
 
 slc_status slc_fast_checks(slc_plan* p, const slc_payload_hdr* hdrs, const void* const* recs, int32_t R,
@@ -850,6 +892,8 @@ void slc_plan_destroy(slc_plan* p) {
     if (p->d_tmaps) cudaFree(p->d_tmaps);
     if (p->d_utmaps) cudaFree(p->d_utmaps);
     if (p->d_wire_off) cudaFree(p->d_wire_off);
+    if (p->d_rec_extra) cudaFree(p->d_rec_extra);
+    if (p->d_pc_scratch) cudaFree(p->d_pc_scratch);
     if (p->d_binom) cudaFree(p->d_binom);
   }
   delete p;

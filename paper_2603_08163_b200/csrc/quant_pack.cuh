@@ -75,7 +75,8 @@ struct QuantOut {
 template <int KC = 0, int IBC = 0>
 __device__ __forceinline__ QuantOut warp_quantize_pack(const uint32_t* selpos, const float* selval,
                                                        uint32_t* selcode, int k_rt, int k_eff, const Geom& g,
-                                                       uint32_t* rec, uint32_t* err) {
+                                                       uint32_t* rec, uint32_t* err, const uint64_t* extra = nullptr,
+                                                       int n_extra = 0, int64_t rec_word = 0) {
   const int lane = threadIdx.x & 31;
   const int k = KC ? KC : k_rt;
   const int W = (k + 31) >> 5;
@@ -133,6 +134,10 @@ __device__ __forceinline__ QuantOut warp_quantize_pack(const uint32_t* selpos, c
       word = scale_word;
     }
     rec[wi] = word;
+    // the same record pushed to every extra destination (slc_compress_multi:
+    // e.g. each rank's peer message over NVLink — the a8 all-gather folded
+    // into the compress kernel)
+    for (int e = 0; e < n_extra; e++) reinterpret_cast<uint32_t*>(__ldg(extra + e))[rec_word + wi] = word;
   }
   return q;
 }

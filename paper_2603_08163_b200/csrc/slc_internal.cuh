@@ -66,7 +66,12 @@ struct CompressArgs {
   float beta;
   int64_t max_ld;  // largest row length of a blocked chunk (32-bit in-chunk offsets if small)
   Geom g;
+  // slc_compress_multi: n_extra more record buffers (device array of pointers,
+  // e.g. NVLink peer memory) receive the same records at the same offsets
+  const uint64_t* rec_extra;
+  int n_extra;
 };
+constexpr int kMaxRecOut = 16;
 
 enum AggMode : int { kAggOnly = 0, kUpdateFromAgg = 1, kFused = 2 };
 
@@ -152,5 +157,9 @@ __device__ __forceinline__ double peer_weight(const AggArgs& a, int i) {
 }
 #endif
 bool compress_supported(int C);
+// a8 / a9 over NVLink peer memory: copy up to kMaxPeers byte ranges in one kernel
+cudaError_t launch_peer_copy(const void* const* src, void* const* dst, const int64_t* bytes, int n, void* dev_scratch,
+                             cudaStream_t s);
+size_t peer_copy_scratch_bytes();
 
 }  // namespace slc

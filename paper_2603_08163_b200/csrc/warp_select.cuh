@@ -229,6 +229,8 @@ struct Compressor {
   float* ef;
   uint32_t* records;
   uint32_t* err;
+  const uint64_t* rec_extra;
+  int n_extra;
   Geom g;
   int64_t n_elems, n_chunks;
   WarpScratch<C, CAP, KMAX>& ws;
@@ -239,6 +241,8 @@ struct Compressor {
       : ef(a.ef),
         records(a.records),
         err(a.err),
+        rec_extra(a.rec_extra),
+        n_extra(a.n_extra),
         g(a.g),
         n_elems(a.n_elems),
         n_chunks(a.n_chunks),
@@ -417,7 +421,8 @@ struct Compressor {
     SLC_CHECK(s.c >= 0 && s.c < n_chunks, "stage_Q chunk");
     SLC_CHECK(s.k_eff >= 1 && s.k_eff <= KMAX, "stage_Q k_eff");
     s.q = warp_quantize_pack<KC, IBC>(ws.selpos, ws.selval, ws.code, k, s.k_eff, g,
-                                      records + s.c * g.rec_words, err);
+                                      records + s.c * g.rec_words, err, rec_extra, n_extra,
+                                      s.c * g.rec_words);
   }
 
   __device__ __forceinline__ void stage_F(const Sel& s) {

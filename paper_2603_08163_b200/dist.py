@@ -71,6 +71,50 @@ class PayloadGather:
         return message[g * self.slot:g * self.slot + self.sizes[g]]
 
 
+class PeerMessage:
+    """a8 over NVLink peer memory, folded into the compress kernel: the peer
+    message (world * slot bytes, rank g's records at g * slot) lives in
+    symmetric memory on every rank, and slc_compress_multi stores each record
+    both into the rank's own slot and, through the NVLink peer mappings, into
+    the same slot of every other rank's message — no separate collective.  A
+    device-side barrier (symmetric-memory signal pads) then tells every rank
+    that all shards have landed (`wait`).  The own slot doubles as the rank's
+    records buffer for the fused update."""
+
+    def __init__(self, plan: slc.Plan, group=None):
+        import torch.distributed._symmetric_memory as symm
+        self.plan = plan
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.sizes = shard_payloads(plan.layout, plan.geom, self.world, plan.dtype)
+        self.slot = (max(self.sizes) + 15) // 16 * 16
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.message = symm.empty(self.world * self.slot, dtype=torch.uint8, device=dev)
+        self.message.zero_()
+        self.handle = symm.rendezvous(self.message, self.group.group_name)
+        base = [int(self.handle.buffer_ptrs[g]) for g in range(self.world)]
+        own = self.rank * self.slot
+        # own slot first (the binding size-checks it), then the same slot of every other rank's message
+        self.records = self.message[own:own + self.slot]
+        self._outs = [self.records] + [base[g] + own for g in range(self.world) if g != self.rank]
+
+    def compress(self, theta, theta_local, ef, beta: float = 0.95, stream=None):
+        self.plan.compress_multi(theta, theta_local, ef, self._outs, beta=beta, stream=stream)
+
+    def wait(self, stream=None):
+        """Every rank's records are in every message (device-side barrier on `stream`)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.handle.barrier(channel=0)
+
+    def slice_of(self, g: int) -> torch.Tensor:
+        return self.message[g * self.slot:g * self.slot + self.sizes[g]]
+
+    def contiguous_message(self) -> torch.Tensor:
+        return torch.cat([self.slice_of(g) for g in range(self.world)])
+
+
 class PeerExchange:
     """a9: peer r's (padded) message lives on rank r % n; every rank receives
     its own slice of every message.
@@ -143,6 +187,52 @@ class PeerExchange:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         return [s[:self.g.sizes[rank]] for s in self.slices]
+
+
+class PeerExchangeP2P:
+    """a9 over NVLink peer memory: the owners' staged messages live in symmetric
+    memory; after a device barrier every rank PULLS its slice of every peer's
+    message straight from the owner with one slc_peer_copy kernel (all SMs, all
+    links at once), then a second barrier lets the owners re-stage."""
+
+    def __init__(self, plan: slc.Plan, sizes, slot: int, n_peers: int, group=None):
+        import torch.distributed._symmetric_memory as symm
+        self.plan = plan
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.sizes, self.slot, self.n_peers = list(sizes), slot, n_peers
+        self.n_own_max = (n_peers + self.world - 1) // self.world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.store = symm.empty(max(1, self.n_own_max) * self.world * slot, dtype=torch.uint8, device=dev)
+        self.handle = symm.rendezvous(self.store, self.group.group_name)
+        self.base = [int(self.handle.buffer_ptrs[g]) for g in range(self.world)]
+        self.recv = torch.zeros(n_peers * slot, dtype=torch.uint8, device=dev)
+        mine = self.sizes[self.rank]
+        msg = self.world * slot
+        self.pairs = [(self.base[r % self.world] + (r // self.world) * msg + self.rank * slot,
+                       self.recv.data_ptr() + r * slot, mine) for r in range(n_peers)]
+
+    def stage(self, i: int, message: torch.Tensor):
+        """Owned peer i's full padded message (peer r = rank + i*world), as the download would write it."""
+        msg = self.world * self.slot
+        self.store[i * msg:(i + 1) * msg].copy_(message[:msg])
+
+    def exchange(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.handle.barrier(channel=0)   # every owner has staged its messages
+            self.plan.peer_copy(self.pairs, stream=s)
+            self.handle.barrier(channel=1)   # every pull has finished reading
+
+    def slice(self, r: int) -> torch.Tensor:
+        return self.recv[r * self.slot:r * self.slot + self.sizes[self.rank]]
+
+    def run(self, owned_messages: Sequence[torch.Tensor]):
+        for i, m in enumerate(owned_messages):
+            self.stage(i, m)
+        self.exchange()
+        return [self.slice(r) for r in range(self.n_peers)]
 
 
 class MedianNorm:

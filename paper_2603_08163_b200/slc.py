@@ -71,6 +71,8 @@ def _load():
         "slc_record_bytes": (ctypes.c_int64, [pp(Geometry)]),
         "slc_layout_digest": (ctypes.c_int, [pp(Geometry), pp(Tensor), ctypes.c_int32, P]),
         "slc_compress": (ctypes.c_int, [P, P, P, P, ctypes.c_float, P, P]),
+        "slc_compress_multi": (ctypes.c_int, [P, P, P, P, ctypes.c_float, P, ctypes.c_int32, P]),
+        "slc_peer_copy": (ctypes.c_int, [P, P, P, P, ctypes.c_int32, P]),
         "slc_compress_range": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int64, P, P, P, ctypes.c_float, P, P]),
         "slc_decode_aggregate": (ctypes.c_int, [P, P, P, ctypes.c_int32, P, P, P]),
         "slc_outer_update": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, P, ctypes.c_float, P]),
@@ -107,7 +109,8 @@ EXPORTED = ["slc_plan_create", "slc_plan_info_get", "slc_plan_segment", "slc_rec
             "slc_median_norm_weights", "slc_decode_aggregate_wdev", "slc_outer_update_wdev", "slc_wire_layout",
             "slc_wire_encode", "slc_wire_decode", "slc_wire_header_write", "slc_wire_header_read", "slc_get_status",
             "slc_plan_destroy", "slc_status_string", "slc_index_rank", "slc_plan_set_option",
-            "slc_fast_checks", "slc_ec_record_bytes", "slc_index_encode", "slc_index_decode"]
+            "slc_fast_checks", "slc_ec_record_bytes", "slc_index_encode", "slc_index_decode", "slc_compress_multi",
+            "slc_peer_copy"]
 
 # slc_fast_checks flag bits (include/slc.h)
 CHECK_LIVENESS, CHECK_SYNC, CHECK_FINITE, CHECK_NORM = 1, 2, 4, 8
@@ -275,6 +278,23 @@ class Plan:
         self._check_bytes(records, self.payload_bytes, "records")
         _check(_lib.slc_compress(self._h, _dptr(theta), _dptr(theta_local), _dptr(ef), ctypes.c_float(beta),
                                  _dptr(records), _stream_ptr(stream)), "slc_compress")
+
+    def compress_multi(self, theta, theta_local, ef, records_out: Sequence, beta: float = 0.95, stream=None) -> None:
+        """slc_compress writing the records to every buffer of records_out (tensors, or raw device
+        addresses as ints for peer mappings); records_out[0] must be a tensor (size-checked)."""
+        self._check_dense(theta, theta_local, ef)
+        self._check_bytes(records_out[0], self.payload_bytes, "records")
+        ptrs = (ctypes.c_void_p * len(records_out))(*[r if isinstance(r, int) else r.data_ptr() for r in records_out])
+        _check(_lib.slc_compress_multi(self._h, _dptr(theta), _dptr(theta_local), _dptr(ef), ctypes.c_float(beta),
+                                       ptrs, len(records_out), _stream_ptr(stream)), "slc_compress_multi")
+
+    def peer_copy(self, pairs, stream=None) -> None:
+        """Rows a8 / a9: copy [(src, dst, nbytes)] (device addresses as ints, peer mappings allowed) in one kernel."""
+        n = len(pairs)
+        src = (ctypes.c_void_p * max(1, n))(*[int(a) for a, _, _ in pairs])
+        dst = (ctypes.c_void_p * max(1, n))(*[int(b) for _, b, _ in pairs])
+        nb = (ctypes.c_int64 * max(1, n))(*[int(c) for _, _, c in pairs])
+        _check(_lib.slc_peer_copy(self._h, src, dst, nb, n, _stream_ptr(stream)), "slc_peer_copy")
 
     def compress_range(self, chunk_begin: int, n_chunks: int, theta, theta_local, ef, records, beta: float = 0.95,
                        stream=None) -> None:

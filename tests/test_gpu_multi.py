@@ -81,11 +81,37 @@ def _worker(rank, world, port, layout_name, dtype, R, sample, q):
                 ref, _, _ = oracle_compress_shard(full, layout, seed, r, dtype, special_period=16, warm_ef=True)
                 ok &= np.array_equal(full_recs[r].cpu().numpy().view(np.uint32), ref)
             res["a8_oracle"] = ok
+        # a8 over NVLink peer memory: compress pushes every record into every rank's message
+        try:
+            from paper_2603_08163_b200.dist import PeerMessage
+            pm = PeerMessage(plan)
+            ok = True
+            for r in range(R):
+                th_, tl_, ef_ = make_device_inputs(plan, layout, seed, r, dtype, special_period=16, warm_ef=True,
+                                                   theta=theta)
+                pm.compress(th_, tl_, ef_)
+                pm.wait()
+                torch.cuda.synchronize()
+                ok &= torch.equal(pm.contiguous_message(), full_recs[r])
+                dist.barrier()
+            res["a8_p2p"] = ok
+        except Exception:
+            import traceback
+            res["a8_p2p_error"] = traceback.format_exc()[-1500:]
         # a9: peer r's padded message lives on rank r % world
         ex = PeerExchange(gather, R)
         slices = ex.run([messages[r] for r in range(rank, R, world)])
         torch.cuda.synchronize()
         res["a9"] = all(torch.equal(s, o) for s, o in zip(slices, own))
+        try:  # a9 pulled over NVLink peer memory
+            from paper_2603_08163_b200.dist import PeerExchangeP2P
+            exp = PeerExchangeP2P(plan, gather.sizes, gather.slot, R)
+            sl2 = exp.run([messages[r] for r in range(rank, R, world)])
+            torch.cuda.synchronize()
+            res["a9_p2p"] = all(torch.equal(s, o) for s, o in zip(sl2, own))
+        except Exception:
+            import traceback
+            res["a9_p2p_error"] = traceback.format_exc()[-1500:]
         # e: fused outer step on the shard vs the oracle
         alpha = 0.65
         th0 = theta.clone()
@@ -171,7 +197,7 @@ def test_nccl_gather_exchange_update(world, layout_name, dtype, R, sample):
     res = [q.get(timeout=900) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
-    errs = [r["error"] for r in res if "error" in r]
+    errs = [r[k] for r in res for k in r if k.endswith("error")]
     assert not errs, errs[0]
     for r in res:
         for k, v in r.items():
