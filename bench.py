@@ -375,9 +375,18 @@ def run_slc(args):
         "hbm_frac_of_peak": step_gbs_rank / peak,
         "roofline": {"bound": "hbm", "kernel": "slc_compress", "achieved": comp_gbs, "peak": peak,
                      "unit": "GB/s", "frac": comp_gbs / peak,
+                     "frac_of_8tbs": comp_gbs / 8000.0,
                      "traffic": (ncu_traffic("compress", wl) if R == WORKLOADS[wl][1] and args.block == 64
                                  and args.k == 64 and not args.shard_of else None),
+                     "traffic_source": ("not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum "
+                                        "per launch from the committed ncu --set full capture "
+                                        "(profiles/ncu_traffic.json) of the same kernel on this workload"),
                      "algorithmic_bytes_per_launch": comp_bytes, "peak_source": peak_src},
+        "step_roofline": {"achieved_gbs_per_gpu": step_gbs_rank, "frac_of_measured_peak": step_gbs_rank / peak,
+                          "frac_of_8tbs": step_gbs_rank / 8000.0,
+                          "bytes_per_param": (comp_bytes + upd_bytes) / max(1, n_local),
+                          "note": "whole step (compress + fused update) algorithmic bytes / step time, per GPU; "
+                                  "north_star's roofline is 8 TB/s per GPU"},
         "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
                     "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
         "gpu_launches": ((4 if args.median_norm else 2)
@@ -592,12 +601,56 @@ def run_e2e(args, plan, shard, recs, stream):
 
 
 # --------------------------------------------------------------------------- oracle (CPU) arm
+_CPU_SAMPLE = None  # the oracle sample, inherited by forked workers
+
+
+def _oracle_worker(args):
+    """One host core: cycle over its share of the sample for `seconds`."""
+    wid, nworkers, seconds = args
+    import oracle
+    g = oracle.geom()
+    mine = _CPU_SAMPLE[wid::nworkers] or _CPU_SAMPLE[:1]
+    work, steps, params = 0.0, 0, 0
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end:
+        for a, l, e, peers, n in mine:
+            t0 = time.perf_counter()
+            st, rec, en = oracle.compress_chunk(a, l, e, BETA, g)
+            delta = oracle.aggregate_chunk([rec] + peers, n, g=g)
+            oracle.outer_update(a, delta, ALPHA)
+            work += time.perf_counter() - t0
+            steps += 1
+            params += n
+            if time.perf_counter() >= t_end:
+                break
+    return work, steps, params
+
+
+def _cpu_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    aff = sorted(os.sched_getaffinity(0))
+    return model, os.cpu_count(), aff
+
+
 def cpu_baseline(layout, R, dtype, seconds, pool=256):
-    """The oracle as it stands (oracle/slco.c, single-threaded) on a bounded
-    sample of the workload: per chunk-step = compress the own chunk + aggregate
-    R records (own + R-1 peers) + outer update, over a deterministic pool of
-    `pool` chunks drawn across all tensors (peer records precomputed, untimed),
-    cycled until `seconds` of oracle time.  params/s = chunk params / time."""
+    """The oracle as it stands (oracle/slco.c, single-threaded C, untuned) on a
+    bounded sample of the workload, on every host core of this process's
+    affinity mask: per chunk-step = compress the own chunk + aggregate R
+    records (own + R-1 peers) + outer update, over a deterministic pool of
+    `pool` chunks drawn across all tensors (peer records precomputed, untimed);
+    chunks are independent, so T forked workers each cycle over a
+    disjoint share for `seconds` of wall time.  params/s = all params done /
+    wall time.  A single-core run of seconds/4 is reported beside it."""
+    global _CPU_SAMPLE
+    import multiprocessing as mp
+
     import numpy as np
 
     import oracle
@@ -621,26 +674,26 @@ def cpu_baseline(layout, R, dtype, seconds, pool=256):
                                                slcgen.generate_at(2, 0, r, G, warm_ef=True), BETA, g)
             peers.append(rec)
         sample.append((a, l, e, peers, len(off)))
-    work, steps, params = 0.0, 0, 0
-    while work < seconds:
-        for a, l, e, peers, n in sample:
-            t0 = time.perf_counter()
-            st, rec, en = oracle.compress_chunk(a, l, e, BETA, g)
-            delta = oracle.aggregate_chunk([rec] + peers, n, g=g)
-            oracle.outer_update(a, delta, ALPHA)
-            work += time.perf_counter() - t0
-            steps += 1
-            params += n
-            if work >= seconds:
-                break
-    return {"value": params / work, "unit": "params/s", "cores": 1, "kind": "oracle",
+    _CPU_SAMPLE = sample
+    model, ncpu, aff = _cpu_info()
+    T = max(1, len(aff))
+    w1, s1, p1 = _oracle_worker((0, 1, max(1.0, seconds / 4)))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(T) as pl:
+        res = pl.map(_oracle_worker, [(w, T, seconds) for w in range(T)])
+    wall = time.perf_counter() - t0
+    steps = sum(r[1] for r in res)
+    params = sum(r[2] for r in res)
+    return {"value": params / wall, "unit": "params/s", "cores": T, "kind": "oracle",
             "sample": f"{steps} chunk-steps over a pool of {len(sample)} chunks drawn from all {len(layout)} tensors "
-                      f"({params} params), R={R}; per chunk: compress own + aggregate R records + update; "
-                      f"single-threaded C oracle, {work:.1f} s"}
+                      f"({params} params), R={R}; per chunk: compress own + aggregate R records + update; the "
+                      f"single-threaded C oracle on {T} forked workers (disjoint chunk shares), {wall:.1f} s wall",
+            "single_thread_value": p1 / w1, "single_thread_seconds": w1,
+            "cpu_model": model, "cpu_count": ncpu, "affinity": aff, "wall_seconds": wall}
 
 
 def run_reference(args):
-    """--impl reference: the oracle (this tier's reference arm) on host cores."""
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
     rank, world, local = dist_env()
     if rank != 0:
         return None
@@ -654,17 +707,20 @@ def run_reference(args):
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(layout, R, dtype, per_step)
+        cb = cpu_baseline(layout, R, dtype, per_step, pool=128)
         if i >= args.warmup:
             vals.append(cb["value"])
     v = statistics.median(vals)
     P = slcgen.layouts.total_params(layout)
     return {"impl": "reference", "metric": "outer-step params/s", "value": v, "unit": "params/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": P / v * 1e3,
+            "extrapolated": True,
+            "extrapolation": f"each step runs the oracle on a bounded sample ({cb['sample']}); ms_per_step = "
+                             f"{P} params / the measured params/s (a full step would take {P / v:.0f} s)",
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic (slcgen)",
             "config": {"workload": f"{wl} ({P} params), R={R} peers, C=4096 k=64 2-bit", "params": P, "peers": R},
-            "cpu_baseline": {"value": v, "unit": "params/s", "cores": 1, "kind": "oracle", "sample": cb["sample"]},
+            "cpu_baseline": {**cb, "value": v},
             "e2e": {"value": v, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
