@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run shard --shard-rank of an N-way FSDP sharding (one GPU's share of a larger job)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--cold-ef", action="store_true", help="round 0: e = 0 (with bf16 params many magnitudes tie)")
     ap.add_argument("--special-period", type=int, default=0,
                     help="1/P of the 4096-element runs degenerate (zero, constant, ties, ...; slcgen)")
     ap.add_argument("--block", type=int, default=64, help="chunk side B (C = B*B; P:88 uses 64)")
@@ -244,7 +245,7 @@ def run_slc(args):
             pmsg = sdist.PeerMessage(plan)
         gather = sdist.PayloadGather(plan)  # also the a8 reference timing in `collectives`
     own_records = pmsg.records if pmsg is not None else (gather.alloc_records() if gather else None)
-    shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=True, records=own_records)
+    shard = ShardState(plan, layout, seed=0, peer=0, dtype=dtype, warm_ef=not args.cold_ef, records=own_records)
     peers = make_peer_records(plan, layout, shard, seed=0, n_peers=R - 1, first_peer=1, dtype=dtype)
     shard.reset()
     recs = [shard.records[:plan.payload_bytes]] + peers
@@ -401,6 +402,8 @@ def run_slc(args):
                                        **time_offload(offload, stream, reps=3)}
     if args.special_period:
         out["config"]["special_period"] = args.special_period
+    if args.cold_ef:
+        out["config"]["ef"] = "cold (round 0, e = 0)"
     if args.median_norm:
         out["config"]["median_norm"] = ("P:101: exact payload norms (slc_payload_sqnorm) + int64 all-reduce + "
                                         "lower-median weights on device + weighted fused update; in the timed step")

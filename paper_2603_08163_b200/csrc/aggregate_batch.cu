@@ -73,8 +73,6 @@ namespace {
 constexpr int kC = 4096, kK = 64, kIB = 12, kRW = 29, kNT = SLC_BATCH_NT;
 constexpr int kNW = kNT / 32;
 constexpr int kMinBlocks = kNT >= 512 ? 2 : 3;
-constexpr int kRPQ = 16, kRPQ_SHIFT = 4;  // 4-element groups per 64-wide block row
-constexpr int kMaxNB = 4;
 constexpr int kMaxR = 64;
 
 enum : int { kFast = 0, kPair = 1, kSeqW = 2 };

@@ -69,6 +69,19 @@ __device__ __forceinline__ void load_f32x4(const float* base, int64_t off, int n
   }
 }
 
+// the same through L2 with the normal eviction policy (ld.global.cg): the
+// selection fallbacks re-read a chunk's candidate groups several times
+__device__ __forceinline__ void load_f32x4_l2(const float* base, int64_t off, int n, float v[4]) {
+  const float* p = base + off;
+  if (n == 4) {
+    float4 u = __ldcg(reinterpret_cast<const float4*>(p));
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; j++) v[j] = j < n ? __ldcg(p + j) : 0.0f;
+  }
+}
+
 __device__ __forceinline__ void store_f32x4(float* base, int64_t off, int n, const float v[4]) {
   float* p = base + off;
   if (n == 4) {

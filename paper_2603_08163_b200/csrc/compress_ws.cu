@@ -41,6 +41,9 @@ using namespace wsel;
 #ifndef SLC_WS_CAPG
 #define SLC_WS_CAPG 256  // candidate capacity of the any-geometry instantiation (k != 64)
 #endif
+#ifndef SLC_WS_CAP64
+#define SLC_WS_CAP64 128  // candidate capacity of the paper's geometry (C 4096, k 64)
+#endif
 #ifndef SLC_WS_XS
 #define SLC_WS_XS 0  // hand-off slots beyond one per warp
 #endif
@@ -270,7 +273,7 @@ __device__ __forceinline__ void stream_warp(const CompressArgs& a, Smem& sm, int
 template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int NSEL, int NS, class Smem>
 __device__ __forceinline__ void select_warp(const CompressArgs& a, Smem& sm, int sel, int lane) {
   constexpr int NP = WarpCfg<C>::NP;
-  Compressor<C, BF16, KC, IBC, CAP, KMAX> cp(a, sm.scratch[sel], lane, KC ? KC : a.g.k);
+  Compressor<C, BF16, KC, IBC, CAP, KMAX, true> cp(a, sm.scratch[sel], lane, KC ? KC : a.g.k);
   const int64_t G = gridDim.x, n = a.n_chunks;
   for (int64_t j = sel;; j += NSEL) {
     const int64_t c = blockIdx.x + j * G;
@@ -311,6 +314,72 @@ __global__ void __launch_bounds__((NSW + NSEL) * 32, 1) compress_ws_kernel(const
     select_warp<C, BF16, KC, IBC, CAP, KMAX, NSEL, NS>(a, sm, warp - NSW, lane);
 }
 
+// The chunks compress_ws_kernel deferred (more than CAP candidates: tied
+// levels, constant or sparse runs; or a non-finite value): one warp per chunk
+// takes T and the candidate groups from the deferral info, re-reads those
+// groups of e = b (stored by the stream) and runs the selection with its
+// fallback chain (key_select / tie_select / radix, warp_select.cuh), then Q
+// and F.  Warp-strided over the list; the last block to finish zeroes the
+// list header for the next launch.
+constexpr int kFbWarps = 4;
+
+// L2 prefetch of a full chunk's e (the warp's next deferred chunk, so its
+// HBM latency hides behind the current one; partial chunks are not prefetched)
+template <int C>
+__device__ __forceinline__ void prefetch_chunk_l2(const float* ef, const ChunkDesc& d, int lane) {
+  if (d.len != C) return;
+  constexpr int B = WarpCfg<C>::B;
+  constexpr int LPR = B * 4 / 128;  // 128-byte lines per block row
+  constexpr int LINES = C * 4 / 128;
+#pragma unroll
+  for (int t = lane; t < LINES; t += 32) {
+    const float* p = d.ld ? ef + d.base + (int64_t)(t / LPR) * d.ld + 32 * (t % LPR) : ef + d.base + 32 * (int64_t)t;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+#ifndef SLC_FB_MINB
+#define SLC_FB_MINB 4  // fallback blocks per SM (register cap 65536 / (32 * kFbWarps * SLC_FB_MINB))
+#endif
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
+__global__ void __launch_bounds__(kFbWarps * 32, SLC_FB_MINB) compress_fallback_kernel(const CompressArgs a) {
+  __shared__ WarpScratch<C, CAP, KMAX> scratch[kFbWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Compressor<C, BF16, KC, IBC, CAP, KMAX, false> cp(a, scratch[warp], lane, KC ? KC : a.g.k);
+  const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&a.defer[0]);
+  const uint32_t* list = a.defer + kDeferHdr;
+  // entries are taken one at a time from a shared counter (a tied chunk's
+  // selection costs several times a plain one), the next one as soon as the
+  // current one starts, so its e can be prefetched into L2 meanwhile
+  auto take = [&]() {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(&a.defer[2], 1u);
+    return __shfl_sync(kFull, i, 0);
+  };
+  uint32_t i = take();
+  while (i < n) {
+    const uint32_t next = take();
+    if (next < n) prefetch_chunk_l2<C>(a.ef, a.chunks[list[next]], lane);
+    Sel s;
+    s.c = list[i];
+    s.d = a.chunks[s.c];
+    s.len = s.d.len;
+    s.full = s.len == C;
+    s.k_eff = s.full ? cp.k : max(1, (cp.k * s.len) / C);
+    cp.select_deferred(s, list + a.defer_cap + (int64_t)i * kDeferInfo);
+    i = next;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.defer[1], 1u) == gridDim.x - 1) {
+      a.defer[0] = 0u;
+      a.defer[1] = 0u;
+      a.defer[2] = 0u;
+      __threadfence();
+    }
+  }
+}
+
 template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
 cudaError_t launch_ws_t(const CompressArgs& a, cudaStream_t s) {
   if (a.max_ld >= (1 << 24)) return launch_compress_warp(a, BF16, s);  // in-chunk offsets need > 32 bits
@@ -326,13 +395,15 @@ cudaError_t launch_ws_t(const CompressArgs& a, cudaStream_t s) {
   int64_t grid = sms;
   if (grid > a.n_chunks) grid = a.n_chunks;
   kern<<<(unsigned)grid, (NSW + NSEL) * 32, smem, s>>>(a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  compress_fallback_kernel<C, BF16, KC, IBC, CAP, KMAX><<<(unsigned)(SLC_FB_MINB * sms), kFbWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int C, bool BF16>
 cudaError_t launch_ws_c(const CompressArgs& a, cudaStream_t s) {
   if (C == 4096 && a.g.k == 64 && a.g.ib == 12)  // the paper's geometry
-    return launch_ws_t<C, BF16, 64, 12, 128, 64>(a, s);
+    return launch_ws_t<C, BF16, 64, 12, SLC_WS_CAP64, 64>(a, s);
   return launch_ws_t<C, BF16, 0, 0, SLC_WS_CAPG, kMaxK>(a, s);
 }
 
@@ -353,8 +424,13 @@ extern "C" int slc_debug_phase_cycles_ws(unsigned long long* out8, int reset) {
   if (reset) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    cudaMemcpyToSymbol(g_path_count, z, sizeof(z));
+    cudaMemcpyToSymbol(g_path_count, z, sizeof(z), sizeof(z));
   }
   return (int)e;
+}
+extern "C" int slc_debug_path_count_ws(unsigned long long* out8) {
+  return (int)cudaMemcpyFromSymbol(out8, g_path_count, sizeof(unsigned long long) * 16);
 }
 #endif
 }  // namespace slc

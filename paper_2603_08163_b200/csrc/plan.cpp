@@ -50,6 +50,7 @@ struct slc_plan {
   uint64_t* d_rec_extra = nullptr;
   int n_extra_next = 0;
   void* d_pc_scratch = nullptr;  // slc_peer_copy's segment table
+  uint32_t* d_defer = nullptr;   // compress: deferred-chunk list (count, blocks done, chunk ids)
   // slc_plan_set_option
   int agg_variant = 0;
   int64_t agg_grid_cap = 0;
@@ -457,6 +458,8 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_wire_off, wire_off.size() * sizeof(int64_t));
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_rec_extra, slc::kMaxRecOut * sizeof(uint64_t));
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_pc_scratch, slc::peer_copy_scratch_bytes());
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_defer, slc::defer_words((int64_t)table.size()) * sizeof(uint32_t));
+    if (ce == cudaSuccess) ce = cudaMemset(p->d_defer, 0, slc::kDeferHdr * sizeof(uint32_t));
     if (ce == cudaSuccess)
       ce = cudaMemcpy(p->d_wire_off, wire_off.data(), wire_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
   }
@@ -464,6 +467,7 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     if (p->d_wire_off) cudaFree(p->d_wire_off);
     if (p->d_rec_extra) cudaFree(p->d_rec_extra);
     if (p->d_pc_scratch) cudaFree(p->d_pc_scratch);
+    if (p->d_defer) cudaFree(p->d_defer);
     if (p->d_err) cudaFree(p->d_err);
     if (p->d_chunks) cudaFree(p->d_chunks);
     if (p->d_tmaps) cudaFree(p->d_tmaps);
@@ -548,6 +552,8 @@ slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* t
   a.g = p->g;
   a.rec_extra = p->d_rec_extra;
   a.n_extra = p->n_extra_next;
+  a.defer = p->d_defer;
+  a.defer_cap = p->n_chunks;
   DeviceGuard guard(p->device);
   cudaStream_t st = use_stream(p, stream);
   if (slc::compress_tma_supported(p->g)) {
@@ -894,6 +900,7 @@ void slc_plan_destroy(slc_plan* p) {
     if (p->d_wire_off) cudaFree(p->d_wire_off);
     if (p->d_rec_extra) cudaFree(p->d_rec_extra);
     if (p->d_pc_scratch) cudaFree(p->d_pc_scratch);
+    if (p->d_defer) cudaFree(p->d_defer);
     if (p->d_binom) cudaFree(p->d_binom);
   }
   delete p;

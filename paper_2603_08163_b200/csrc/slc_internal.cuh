@@ -70,8 +70,19 @@ struct CompressArgs {
   // e.g. NVLink peer memory) receive the same records at the same offsets
   const uint64_t* rec_extra;
   int n_extra;
+  // compress_ws: chunks whose selection leaves the candidate path (more than
+  // CAP candidates, or a non-finite value) are deferred to a second kernel.
+  // defer[0] = count, defer[1] = fallback blocks done, defer[2] = next entry
+  // to take (all zero between launches), defer[kDeferHdr ..] = defer_cap
+  // chunk indices (relative to chunks), then defer_cap entries of kDeferInfo
+  // words (warp_select.cuh stage_R).
+  uint32_t* defer;
+  int64_t defer_cap;
 };
 constexpr int kMaxRecOut = 16;
+constexpr int kDeferHdr = 4;
+constexpr int kDeferInfo = 9;  // T, then one group-mask word per pass (NP <= 8)
+inline int64_t defer_words(int64_t n_chunks) { return kDeferHdr + n_chunks * (1 + kDeferInfo); }
 
 enum AggMode : int { kAggOnly = 0, kUpdateFromAgg = 1, kFused = 2 };
 

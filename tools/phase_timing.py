@@ -15,8 +15,9 @@ from slcgen import layouts  # noqa: E402
 lib = ctypes.CDLL(slc.LIB_PATH)
 layout = layouts.LAYOUTS[sys.argv[1] if len(sys.argv) > 1 else "llama3.2-1b"]
 plan = slc.Plan(layout, geom=slc.geometry(int(os.environ.get("BLOCK", 64)), int(os.environ.get("K", 64))),
-                rank=0, nranks=int(os.environ.get("NRANKS", 1)))
-th, tl, ef = make_device_inputs(plan, layout, 1, 0, warm_ef=True)
+                rank=0, nranks=int(os.environ.get("NRANKS", 1)), dtype=os.environ.get("DTYPE", "f32"))
+th, tl, ef = make_device_inputs(plan, layout, 1, 0, warm_ef=not os.environ.get("COLD"), special_period=int(os.environ.get("SPECIAL", 0)),
+                                dtype=os.environ.get("DTYPE", "f32"))
 rec = torch.zeros(plan.payload_bytes, dtype=torch.uint8, device="cuda")
 buf = (ctypes.c_ulonglong * 8)()
 plan.compress(th, tl, ef, rec)
@@ -27,10 +28,18 @@ a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=Tru
 a.record(); plan.compress(th, tl, ef, rec); b.record(); torch.cuda.synchronize()
 fn(buf, 0)
 n = plan.n_chunks
-names = ["A stream", "S threshold", "B candidates", "R rank+slots", "Q quantise+pack", "F EF fix-ups",
-         "stream: wait empty", "select: wait full"]
+names = ["A stream", "S threshold", "B candidates", "R rank+slots (incl. fallbacks)", "Q quantise+pack",
+         "F EF fix-ups", "stream: wait empty", "select: wait full"]
 tot = sum(buf[i] for i in range(8))
 print(f"kernel {a.elapsed_time(b):.3f} ms, {n} chunks; cycles per chunk per warp:")
 for i, nm in enumerate(names):
     print(f"  {nm:18s} {buf[i] / n:10.0f}  {100 * buf[i] / tot:5.1f}%")
 print(f"  {'total':18s} {tot / n:10.0f}")
+if os.environ.get("WS"):
+    pc = (ctypes.c_ulonglong * 16)()
+    lib.slc_debug_path_count_ws(pc)
+    print("  selection paths (chunks): candidates %d, tie %d, tie->rank %d, radix %d" % tuple(pc[:4]))
+    nt = max(1, pc[1] + pc[2] + pc[3]); nr = max(1, pc[3])
+    print("  cycles per call: tie_select %.0f, radix rounds %.0f, radix mark+fill %.0f; radix chunks: mean G %.1f, mean M %.1f"
+          % (pc[4] / nt, pc[5] / nr, pc[6] / nr, pc[7] / nr, pc[8] / nr))
+    print("  reg_select: %d chunks, %.0f cycles per call" % (pc[9], pc[10] / max(1, pc[9])))
