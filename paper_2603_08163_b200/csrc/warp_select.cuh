@@ -32,7 +32,7 @@ namespace slc {
 __device__ unsigned long long g_phase_cycles[8];
 __device__ unsigned long long g_path_count[16];  // selection paths: candidates, tie, tie->rank, radix; then
                                                  // cycles: 4 tie_select, 5 radix rounds, 6 radix mark+fill; 7 sum G, 8 sum M (radix);
-                                                 // 9 key_select calls, 10 its cycles
+                                                 // 9 key_select calls, 10 its cycles, 11 hist_select -> key_select
 #define PATH_COUNT(i) \
   do {                \
     if ((threadIdx.x & 31) == 0) atomicAdd(&g_path_count[i], 1ull); \
@@ -199,6 +199,9 @@ __device__ __forceinline__ void fill_slots(const float* ef, WarpScratch<C, CAP, 
 // exact k_eff-th largest key by 4 rounds of 8-bit radix select over all positions,
 // then key > K plus the first `need` positions with key == K (lower position wins)
 // (a free function: as a member its `this` would pin the Compressor in local memory)
+#ifndef SLC_RADIX_UB
+#define SLC_RADIX_UB 1  // passes whose loads radix_fallback keeps in flight (measured: 4 spills, slower)
+#endif
 template <int C, int CAP, int KMAX>
 __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
                                             const int len, const bool full, const int k_eff) {
@@ -208,6 +211,7 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
   // only groups whose maximum reaches T can hold a selected value (>= k_eff
   // values are >= T): the other groups are neither loaded nor counted
   const uint32_t gm = ws.gm[lane];
+  constexpr int UB = NP < SLC_RADIX_UB ? NP : SLC_RADIX_UB;
   uint32_t Kth = 0;
   int need = k_eff;
 #ifdef SLC_PHASE_TIMING
@@ -218,35 +222,46 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
     for (int i = lane; i < 256; i += 32) ws.hist[i] = 0u;
     __syncwarp();
     const uint32_t hi_mask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    // UB passes' loads in flight per L2 round trip
 #pragma unroll 1
-    for (int u = 0; u < NP; u++) {
-      const bool act = (gm >> u) & 1u;
-      if (!__any_sync(kFull, act)) continue;
+    for (int u0 = 0; u0 < NP; u0 += UB) {
+      float ev[UB][4][4];
+      int nvs[UB][4];
+      bool any = false;
 #pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const int q = 128 * u + 32 * v + lane;
-        const int nv = act ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
-        float ev[4];
-        load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
+      for (int b = 0; b < UB; b++) {
+        const bool act = u0 + b < NP && ((gm >> (u0 + b)) & 1u);
+        any |= act;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const uint32_t key = key2_of(ev[j]);
-          const bool in = j < nv && (key & hi_mask) == (Kth & hi_mask);
-          const uint32_t dg = (key >> shift) & 255u;
-          // tied runs put the whole warp on one bin: one aggregated add instead
-          // of 32 serialised ones
-          const unsigned m = __ballot_sync(kFull, in);
-          if (m) {
-            const uint32_t dmin = __reduce_min_sync(kFull, in ? dg : 255u);
-            const uint32_t dmax = __reduce_max_sync(kFull, in ? dg : 0u);
-            if (dmin == dmax) {
-              if (lane == __ffs(m) - 1) atomicAdd(&ws.hist[dg], (uint32_t)__popc(m));
-            } else if (in) {
-              atomicAdd(&ws.hist[dg], 1u);
-            }
-          }
+        for (int v = 0; v < 4; v++) {
+          const int q = 128 * (u0 + b) + 32 * v + lane;
+          nvs[b][v] = act ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
+          load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nvs[b][v], ev[b][v]);
         }
       }
+      if (!__any_sync(kFull, any)) continue;
+#pragma unroll
+      for (int b = 0; b < UB; b++)
+#pragma unroll
+        for (int v = 0; v < 4; v++)
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const uint32_t key = key2_of(ev[b][v][j]);
+            const bool in = j < nvs[b][v] && (key & hi_mask) == (Kth & hi_mask);
+            const uint32_t dg = (key >> shift) & 255u;
+            // tied runs put the whole warp on one bin: one aggregated add instead
+            // of 32 serialised ones
+            const unsigned m = __ballot_sync(kFull, in);
+            if (m) {
+              const uint32_t dmin = __reduce_min_sync(kFull, in ? dg : 255u);
+              const uint32_t dmax = __reduce_max_sync(kFull, in ? dg : 0u);
+              if (dmin == dmax) {
+                if (lane == __ffs(m) - 1) atomicAdd(&ws.hist[dg], (uint32_t)__popc(m));
+              } else if (in) {
+                atomicAdd(&ws.hist[dg], 1u);
+              }
+            }
+          }
     }
     __syncwarp();
     // digit D: #(digit > D) < need <= #(digit >= D); lane l holds bins 8l..8l+7
@@ -279,38 +294,48 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
 #endif
   int taken = 0;
 #pragma unroll 1
-  for (int u = 0; u < NP; u++) {
+  for (int u0 = 0; u0 < NP; u0 += UB) {
+    float ev[UB][4][4];
+    int nvs[UB][4];
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
-      // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
-      const int q = 128 * u + 32 * v + lane;
-      const int nv = ((gm >> u) & 1u) ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
-      float ev[4];
-      load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nv, ev);
-      uint32_t tmask = 0, m4 = 0;
+    for (int b = 0; b < UB; b++)
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const uint32_t key = key2_of(ev[j]);
-        if (j < nv && key > Kth) m4 |= 1u << j;
-        if (j < nv && key == Kth) tmask |= 1u << j;
+      for (int v = 0; v < 4; v++) {
+        const int q = 128 * (u0 + b) + 32 * v + lane;
+        nvs[b][v] = (u0 + b < NP && ((gm >> (u0 + b)) & 1u)) ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
+        load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nvs[b][v], ev[b][v]);
       }
-      const int tc = __popc(tmask);
-      int o = taken + warp_excl_scan(tc);
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if ((tmask >> j) & 1u) {
-          if (o < need) m4 |= 1u << j;
-          o++;
+    for (int b = 0; b < UB; b++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        // lanes hold consecutive 4-position groups: ascending position = (u, v, lane, j)
+        const int q = 128 * (u0 + b) + 32 * v + lane;
+        const int nv = nvs[b][v];
+        uint32_t tmask = 0, m4 = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t key = key2_of(ev[b][v][j]);
+          if (j < nv && key > Kth) m4 |= 1u << j;
+          if (j < nv && key == Kth) tmask |= 1u << j;
         }
+        const int tc = __popc(tmask);
+        int o = taken + warp_excl_scan(tc);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          if ((tmask >> j) & 1u) {
+            if (o < need) m4 |= 1u << j;
+            o++;
+          }
+        }
+        taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
+        // positions 4q..4q+3 of lanes 8i..8i+7 form bitmap word q >> 3: one store
+        uint32_t wv = m4 << (4 * (lane & 7));
+        wv |= __shfl_xor_sync(kFull, wv, 1);
+        wv |= __shfl_xor_sync(kFull, wv, 2);
+        wv |= __shfl_xor_sync(kFull, wv, 4);
+        if ((lane & 7) == 0 && wv) ws.bit[q >> 3] = wv;
       }
-      taken += (int)__reduce_add_sync(kFull, (unsigned)tc);
-      // positions 4q..4q+3 of lanes 8i..8i+7 form bitmap word q >> 3: one store
-      uint32_t wv = m4 << (4 * (lane & 7));
-      wv |= __shfl_xor_sync(kFull, wv, 1);
-      wv |= __shfl_xor_sync(kFull, wv, 2);
-      wv |= __shfl_xor_sync(kFull, wv, 4);
-      if ((lane & 7) == 0 && wv) ws.bit[q >> 3] = wv;
-    }
   }
   __syncwarp();
   fill_slots<C, CAP, KMAX>(ef, ws, lane, d, k_eff);
@@ -519,8 +544,13 @@ __device__ __forceinline__ void rank_select(WarpScratch<C, CAP, KMAX>& ws, const
 // order (R#3, R#4), slots in ascending position (R#5).  Values with key < Tc
 // are never selected (>= k_eff values reach Tc), so the candidate groups hold
 // every selected value and every tie at K*.
+#ifdef SLC_KS_INLINE
+#define SLC_KS_ATTR __forceinline__
+#else
+#define SLC_KS_ATTR __noinline__
+#endif
 template <int C, int CAP, int KMAX>
-__device__ __noinline__ void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+__device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
                                         const int len, const int k_eff, const int G, const uint32_t Tc, const int M) {
   using K = WarpCfg<C>;
   using WS = WarpScratch<C, CAP, KMAX>;
@@ -609,6 +639,136 @@ __device__ __noinline__ void key_select(float* ef, WarpScratch<C, CAP, KMAX>* ws
   fill_slots<C, CAP, KMAX>(ef, ws, lane, d, k_eff);
 }
 
+// ---- more than XCAP candidates (large k against the 32*NP group maxima, so
+// T is weak, or wide tied levels): one histogram pass over the candidate
+// groups narrows the candidates to the bin holding the k_eff-th key.  Bins
+// are 1/16 binade wide (key bits 30..19 above Tc's), 256 of them, the top one
+// open-ended.  If that bin and the ones above hold at most XCAP values, a
+// second pass collects their keys (as stage B does) and key_select finishes
+// with T' = the bin's lower edge; otherwise false (tie_select / radix).
+#ifndef SLC_HIST_BR
+#define SLC_HIST_BR 1  // candidate groups per lane per L2 round trip in hist_select's counting pass
+#endif
+template <int C, int CAP, int KMAX>
+__device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+                                         const int len, const int k_eff, const int G, const uint32_t Tc) {
+  using K = WarpCfg<C>;
+  using WS = WarpScratch<C, CAP, KMAX>;
+  constexpr int NP = K::NP;
+  constexpr int BR = SLC_HIST_BR;
+  static_assert(2 * CAP >= 256, "hist_select keeps its histogram in ws.cand");
+  WS& ws = *wsp;
+  const bool full = len == C;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws.cand);
+  const uint32_t base = Tc & ~0xFFFFFu;
+  for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+  __syncwarp();
+  // the candidate groups, BR per lane per L2 round trip; f(key, position) per valid value
+  auto walk = [&](auto&& f) {
+#pragma unroll 1
+    for (int r0 = 0; r0 < G; r0 += 32 * BR) {
+      float vals[BR][16];
+      int qb[BR];
+#pragma unroll
+      for (int bq = 0; bq < BR; bq++) {
+        const int gi = r0 + 32 * bq + lane;
+        qb[bq] = -1;
+        if (gi < G) {
+          const uint32_t id = ws.hist[gi];
+          qb[bq] = 128 * (int)(id % NP) + (int)(id / NP);
+#pragma unroll
+          for (int v = 0; v < 4; v++)
+            load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb[bq] + 32 * v),
+                          full ? 4 : valid_in_group(4 * (qb[bq] + 32 * v), len), &vals[bq][4 * v]);
+        }
+      }
+#pragma unroll
+      for (int bq = 0; bq < BR; bq++) {
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int p0 = 4 * (qb[bq] + 32 * v);
+          const int nv = qb[bq] < 0 ? 0 : (full ? 4 : valid_in_group(p0, len));
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (j < nv) f(key2_of(vals[bq][4 * v + j]), p0 + j, vals[bq][4 * v + j]);
+        }
+      }
+    }
+  };
+  walk([&](uint32_t key, int, float) {
+    if (key >= Tc) atomicAdd(&hist[min((key - base) >> 20, 255u)], 1u);
+  });
+  __syncwarp();
+  // bin D: #(bin > D) < k_eff <= #(bin >= D); lane l holds bins 8l..8l+7
+  uint32_t h[8];
+  uint32_t s8 = 0;
+#pragma unroll
+  for (int x = 0; x < 8; x++) { h[x] = hist[8 * lane + x]; s8 += h[x]; }
+  uint32_t inc = s8;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(kFull, inc, o);
+    if (lane + o < 32) inc += y;
+  }
+  uint32_t acc = inc - s8;
+  int found = -1;
+  uint32_t found_ge = 0;
+#pragma unroll
+  for (int x = 7; x >= 0; x--) {
+    if (found < 0 && acc < (uint32_t)k_eff && acc + h[x] >= (uint32_t)k_eff) { found = 8 * lane + x; found_ge = acc + h[x]; }
+    acc += h[x];
+  }
+  const int src = __ffs(__ballot_sync(kFull, found >= 0)) - 1;
+  const uint32_t D = (uint32_t)__shfl_sync(kFull, found, src);
+  const int M2 = (int)__shfl_sync(kFull, found_ge, src);
+  if (M2 > WS::XCAP) return false;
+  const uint32_t T2 = max(Tc, base + (D << 20));
+  __syncwarp();  // the histogram (ws.cand) is read; the candidates overwrite it
+  int M = 0;
+#pragma unroll 1
+  for (int r0 = 0; r0 < G; r0 += 32) {
+    const int gi = r0 + lane;
+    float vals[16];
+    int qb = -1;
+    uint32_t cmask = 0;
+    if (gi < G) {
+      const uint32_t id = ws.hist[gi];
+      qb = 128 * (int)(id % NP) + (int)(id / NP);
+#pragma unroll
+      for (int v = 0; v < 4; v++)
+        load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb + 32 * v), full ? 4 : valid_in_group(4 * (qb + 32 * v), len),
+                      &vals[4 * v]);
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int nv = full ? 4 : valid_in_group(4 * (qb + 32 * v), len);
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (j < nv && key2_of(vals[4 * v + j]) >= T2) cmask |= 1u << (4 * v + j);
+      }
+    }
+    const int cc = __popc(cmask);
+    int o = M + warp_excl_scan(cc);
+    M += (int)__reduce_add_sync(kFull, (unsigned)cc);
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      if ((cmask >> j) & 1u) {
+        const int p = 4 * (qb + 32 * (j >> 2)) + (j & 3);
+        if (o < CAP) {
+          ws.cand[o] = ((uint64_t)key2_of(vals[j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
+          ws.candb[o] = vals[j];
+        } else if (o < WS::XCAP) {
+          ws.xkey[o - CAP] = key2_of(vals[j]);
+        }
+        o++;
+      }
+    }
+  }
+  __syncwarp();
+  SLC_CHECK(M == M2, "hist_select candidates");
+  key_select<C, CAP, KMAX>(ef, wsp, lane, d, len, k_eff, G, T2, M);
+  return true;
+}
+
 // every selection that the candidate path cannot finish (a free, non-inlined
 // function: the common path keeps its registers).  Returns 0 when ws.selpos /
 // selval are complete, else the number of candidates left in ws.cand (<= CAP)
@@ -636,6 +796,10 @@ __device__ __noinline__ int select_fallback(float* ef, WarpScratch<C, CAP, KMAX>
     PATH_ADD(10, clock64() - t0);
 #endif
     PATH_COUNT(9);
+    return 0;
+  }
+  if (!bad && s.G <= 256 && hist_select<C, CAP, KMAX>(ef, wsp, lane, d, len, k_eff, s.G, s.Kmin)) {
+    PATH_COUNT(11);
     return 0;
   }
   if (!bad && s.G <= 256) {

@@ -224,7 +224,8 @@ def test_sharding_invariance(nranks):
     assert torch.equal(torch.cat(parts), rec1.cpu())
 
 
-@pytest.mark.parametrize("block,k", [(32, 16), (64, 16), (64, 32), (64, 128), (64, 256), (128, 256)])
+@pytest.mark.parametrize("block,k", [(32, 4), (32, 16), (32, 64), (64, 16), (64, 32), (64, 128), (64, 256),
+                                     (128, 64), (128, 256)])
 def test_geometry_sweep_parity(block, k, agg_kernel):
     g = slc.geometry(block=block, k=k)
     og = oracle.geom(block=block, k=k)

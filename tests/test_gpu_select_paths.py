@@ -96,9 +96,10 @@ def _to_dev(x, dtype):
     return t.to(DEV)
 
 
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_crafted_selection_paths(dtype):
-    plan = slc.Plan(LAYOUT, dtype=dtype)
+@pytest.mark.parametrize("dtype,block,k", [("f32", 64, 64), ("bf16", 64, 64), ("f32", 64, 256), ("f32", 32, 64),
+                                           ("bf16", 64, 128)])
+def test_crafted_selection_paths(dtype, block, k):
+    plan = slc.Plan(LAYOUT, geom=slc.geometry(block=block, k=k), dtype=dtype)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     theta = torch.zeros(plan.shard_elems, dtype=tdt, device=DEV)
     tl = torch.zeros(plan.shard_elems, dtype=tdt, device=DEV)
@@ -119,7 +120,7 @@ def test_crafted_selection_paths(dtype):
     plan.compress(theta, tl, ef, rec)
     assert plan.get_status() == slc.OK
     got = rec.cpu().numpy().view(np.uint32)
-    g = oracle.geom()
+    g = oracle.geom(block=block, k=k)
     RW = oracle.record_words(g)
     off = 0
     for s, (a, l) in zip(plan.segments, host):

@@ -19,8 +19,8 @@ except SystemExit:
     pass
 pc = (ctypes.c_ulonglong * 16)()
 lib.slc_debug_path_count_ws(pc)
-print("paths over the run: candidates %d, tie %d, tie->rank %d, radix %d, key_select %d" %
-      (pc[0], pc[1], pc[2], pc[3], pc[9]), file=sys.stderr)
+print("paths over the run: candidates %d, tie %d, tie->rank %d, radix %d, key_select %d, hist->key %d" %
+      (pc[0], pc[1], pc[2], pc[3], pc[9], pc[11]), file=sys.stderr)
 nt = max(1, pc[1] + pc[2] + pc[3]); nr = max(1, pc[3])
 print("  cycles per call: tie_select %.0f, radix rounds %.0f, radix mark+fill %.0f, key_select %.0f; "
       "radix chunks: mean G %.1f, mean M %.1f" % (pc[4] / nt, pc[5] / nr, pc[6] / nr, pc[10] / max(1, pc[9]),
