@@ -21,6 +21,8 @@
 // slot to be empty right before writing the maxima, after the whole stream of
 // the chunk.  The release/acquire mbarrier pair also orders the producer's
 // global e stores before the selector's re-reads (same CTA).
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "warp_select.cuh"
 
@@ -67,13 +69,22 @@ struct PassBuf {
   static constexpr int bytes = 512 * (2 * PB + 4);
 };
 
-template <int C, bool BF16, int CAP, int KMAX, int NSW, int NSEL, int D, int NS>
+// hand-off slot: one maximum key per unit and lane; 16-position groups keep
+// the full key, quads (VPU = 1, 4x as many) its upper 16 bits (T stays a
+// lower bound: a truncated maximum never exceeds the true one)
+template <int C, int VPU>
+struct SlotCfg {
+  using T = typename std::conditional<VPU == 1, uint16_t, uint32_t>::type;
+  static constexpr int words = 32 * UnitCfg<C, VPU>::NU;
+};
+
+template <int C, bool BF16, int CAP, int KMAX, int VPU, int NSW, int NSEL, int D, int NS>
 struct WsSmem {
   uint64_t full[NS];
   uint64_t empty[NS];
-  uint32_t gk[NS][32 * WarpCfg<C>::NP];
+  typename SlotCfg<C, VPU>::T gk[NS][SlotCfg<C, VPU>::words];
   unsigned char ring[NSW][D][PassBuf<BF16>::bytes];
-  WarpScratch<C, CAP, KMAX> scratch[NSEL];
+  WarpScratch<C, CAP, KMAX, VPU> scratch[NSEL];
 };
 
 // Per-lane addressing of a FULL chunk: group q = 128u + 32v + lane sits at
@@ -138,9 +149,12 @@ __device__ __forceinline__ void issue_pass(const CompressArgs& a, const ChunkDes
 
 // b of this lane's 4 groups of the pass in buf; returns max |b| (NaN-propagating)
 // over the valid positions, stores e <- b
+// (qdst: quad hand-off — qdst[32 * (4u + v)] = 1 + the upper 16 bits of the
+// quad's maximum key (saturating), 0 for a quad with no valid position)
 template <bool BF16, bool FULL, int RPQ_SHIFT, class Addr>
 __device__ __forceinline__ float consume_pass(const unsigned char* buf, float beta, float* ef, const Addr& la,
-                                              const ChunkDesc& d, int u, int lane, uint64_t pol, int& nvalid) {
+                                              const ChunkDesc& d, int u, int lane, uint64_t pol, int& nvalid,
+                                              uint16_t* qdst = nullptr) {
   using PBuf = PassBuf<BF16>;
   float gm = 0.0f;
 #pragma unroll
@@ -165,11 +179,14 @@ __device__ __forceinline__ float consume_pass(const unsigned char* buf, float be
     const float4 fe = *reinterpret_cast<const float4*>(buf + PBuf::off_e + sl * 16);
     const float ev[4] = {fe.x, fe.y, fe.z, fe.w};
     float b[4];
+    float qm = 0.0f;
 #pragma unroll
     for (int jj = 0; jj < 4; jj++) {
       b[jj] = __fmaf_rn(beta, ev[jj], __fsub_rn(av[jj], lv[jj]));
-      if (FULL || jj < nv) gm = absmax_nan(gm, b[jj]);  // missing positions excluded
+      if (FULL || jj < nv) qm = absmax_nan(qm, b[jj]);  // missing positions excluded
     }
+    gm = absmax_nan(gm, qm);
+    if (qdst) qdst[32 * (4 * u + v)] = (FULL || nv) ? (uint16_t)min((key2_of(qm) >> 16) + 1u, 0xFFFFu) : (uint16_t)0;
     if (FULL) {
       st_f32x4_evict_last(reinterpret_cast<float*>(la.e + la.step(u, v) * 4), b[0], b[1], b[2], b[3], pol);
     } else {
@@ -182,7 +199,7 @@ __device__ __forceinline__ float consume_pass(const unsigned char* buf, float be
   return gm;
 }
 
-template <int C, bool BF16, int NSW, int D, int NS, class Smem>
+template <int C, bool BF16, int VPU, int NSW, int D, int NS, class Smem>
 __device__ __forceinline__ void stream_warp(const CompressArgs& a, Smem& sm, int sw, int lane) {
   using PBuf = PassBuf<BF16>;
   constexpr int NP = WarpCfg<C>::NP;
@@ -228,6 +245,29 @@ __device__ __forceinline__ void stream_warp(const CompressArgs& a, Smem& sm, int
     LaneAddr<C, BF16> la;
     la.init(a, d, lane);
     PHASE_T0();
+    const int slot = (int)(j % NS);
+    const int64_t use = j / NS;
+    if (VPU == 1) {
+      // quads: each pass writes its 4 keys straight into the slot, so the slot
+      // is claimed before the chunk's first pass (it was freed when the chunk
+      // NS back started its selection)
+      if (use > 0) ptx::mbar_wait(&sm.empty[slot], (uint32_t)((use - 1) & 1));
+      uint16_t* qdst = reinterpret_cast<uint16_t*>(&sm.gk[slot][lane]);
+#pragma unroll 1
+      for (int u = 0; u < NP; u++) {
+        cp_async_wait<D - 1>();
+        int nv = 0;
+        if (d.len == C)
+          consume_pass<BF16, true, RPQ_SHIFT>(ring[slot_c], beta, ef, la, d, u, lane, pol_last, nv, qdst);
+        else
+          consume_pass<BF16, false, RPQ_SHIFT>(ring[slot_c], beta, ef, la, d, u, lane, pol_last, nv, qdst);
+        issue_next();
+        slot_c = slot_c + 1 == D ? 0 : slot_c + 1;
+      }
+      PHASE_MARK(0);
+      ptx::mbar_arrive(&sm.full[slot]);  // release: e stores and keys of this lane
+      continue;
+    }
     uint32_t gk[NP];
     // passes not unrolled (instruction-cache footprint: the select warps run
     // other code on the same SM); gk[u] written by predicated moves so the
@@ -258,8 +298,6 @@ __device__ __forceinline__ void stream_warp(const CompressArgs& a, Smem& sm, int
       }
     }
     // hand the maxima over: wait for the slot's previous chunk to be taken
-    const int slot = (int)(j % NS);
-    const int64_t use = j / NS;
     PHASE_MARK(0);
     if (use > 0) ptx::mbar_wait(&sm.empty[slot], (uint32_t)((use - 1) & 1));
     PHASE_MARK(6);
@@ -270,10 +308,10 @@ __device__ __forceinline__ void stream_warp(const CompressArgs& a, Smem& sm, int
   cp_async_wait<0>();
 }
 
-template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int NSEL, int NS, class Smem>
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int VPU, int NSEL, int NS, class Smem>
 __device__ __forceinline__ void select_warp(const CompressArgs& a, Smem& sm, int sel, int lane) {
-  constexpr int NP = WarpCfg<C>::NP;
-  Compressor<C, BF16, KC, IBC, CAP, KMAX, true> cp(a, sm.scratch[sel], lane, KC ? KC : a.g.k);
+  constexpr int NU = UnitCfg<C, VPU>::NU;
+  Compressor<C, BF16, KC, IBC, CAP, KMAX, VPU, true> cp(a, sm.scratch[sel], lane, KC ? KC : a.g.k);
   const int64_t G = gridDim.x, n = a.n_chunks;
   for (int64_t j = sel;; j += NSEL) {
     const int64_t c = blockIdx.x + j * G;
@@ -282,9 +320,14 @@ __device__ __forceinline__ void select_warp(const CompressArgs& a, Smem& sm, int
     PHASE_T0();
     ptx::mbar_wait(&sm.full[slot], (uint32_t)((j / NS) & 1));
     PHASE_MARK(7);
-    uint32_t gk[NP];
+    uint32_t gk[NU];
 #pragma unroll
-    for (int u = 0; u < NP; u++) gk[u] = sm.gk[slot][32 * u + lane];
+    for (int u = 0; u < NU; u++) {
+      // quads: the key rounded down to 16 bits (| 1: a zero quad keeps the key
+      // of 0, as a 16-position group does); 0 = no valid position
+      const uint32_t h = sm.gk[slot][32 * u + lane];
+      gk[u] = VPU == 1 ? (h ? ((h - 1u) << 16) | 1u : 0u) : h;
+    }
     ptx::mbar_arrive(&sm.empty[slot]);
     Sel s;
     s.c = c;
@@ -296,9 +339,9 @@ __device__ __forceinline__ void select_warp(const CompressArgs& a, Smem& sm, int
   }
 }
 
-template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int NSW, int NSEL, int D, int NS>
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int VPU, int NSW, int NSEL, int D, int NS>
 __global__ void __launch_bounds__((NSW + NSEL) * 32, 1) compress_ws_kernel(const CompressArgs a) {
-  using Smem = WsSmem<C, BF16, CAP, KMAX, NSW, NSEL, D, NS>;
+  using Smem = WsSmem<C, BF16, CAP, KMAX, VPU, NSW, NSEL, D, NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -309,9 +352,9 @@ __global__ void __launch_bounds__((NSW + NSEL) * 32, 1) compress_ws_kernel(const
   ptx::fence_mbar_init();
   __syncthreads();
   if (warp < NSW)
-    stream_warp<C, BF16, NSW, D, NS>(a, sm, warp, lane);
+    stream_warp<C, BF16, VPU, NSW, D, NS>(a, sm, warp, lane);
   else
-    select_warp<C, BF16, KC, IBC, CAP, KMAX, NSEL, NS>(a, sm, warp - NSW, lane);
+    select_warp<C, BF16, KC, IBC, CAP, KMAX, VPU, NSEL, NS>(a, sm, warp - NSW, lane);
 }
 
 // The chunks compress_ws_kernel deferred (more than CAP candidates: tied
@@ -340,11 +383,11 @@ __device__ __forceinline__ void prefetch_chunk_l2(const float* ef, const ChunkDe
 #ifndef SLC_FB_MINB
 #define SLC_FB_MINB 4  // fallback blocks per SM (register cap 65536 / (32 * kFbWarps * SLC_FB_MINB))
 #endif
-template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int VPU>
 __global__ void __launch_bounds__(kFbWarps * 32, SLC_FB_MINB) compress_fallback_kernel(const CompressArgs a) {
-  __shared__ WarpScratch<C, CAP, KMAX> scratch[kFbWarps];
+  __shared__ WarpScratch<C, CAP, KMAX, VPU> scratch[kFbWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Compressor<C, BF16, KC, IBC, CAP, KMAX, false> cp(a, scratch[warp], lane, KC ? KC : a.g.k);
+  Compressor<C, BF16, KC, IBC, CAP, KMAX, VPU, false> cp(a, scratch[warp], lane, KC ? KC : a.g.k);
   const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&a.defer[0]);
   const uint32_t* list = a.defer + kDeferHdr;
   // entries are taken one at a time from a shared counter (a tied chunk's
@@ -365,7 +408,7 @@ __global__ void __launch_bounds__(kFbWarps * 32, SLC_FB_MINB) compress_fallback_
     s.len = s.d.len;
     s.full = s.len == C;
     s.k_eff = s.full ? cp.k : max(1, (cp.k * s.len) / C);
-    cp.select_deferred(s, list + a.defer_cap + (int64_t)i * kDeferInfo);
+    cp.select_deferred(s, list + a.defer_cap + (int64_t)i * a.defer_info);
     i = next;
   }
   __syncthreads();
@@ -380,13 +423,14 @@ __global__ void __launch_bounds__(kFbWarps * 32, SLC_FB_MINB) compress_fallback_
   }
 }
 
-template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX>
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int VPU>
 cudaError_t launch_ws_t(const CompressArgs& a, cudaStream_t s) {
   if (a.max_ld >= (1 << 24)) return launch_compress_warp(a, BF16, s);  // in-chunk offsets need > 32 bits
   constexpr int NSW = SLC_WS_NSW, NSEL = SLC_WS_NSEL, D = SLC_WS_D, NS = NSW + NSEL + SLC_WS_XS;
-  using Smem = WsSmem<C, BF16, CAP, KMAX, NSW, NSEL, D, NS>;
+  using Smem = WsSmem<C, BF16, CAP, KMAX, VPU, NSW, NSEL, D, NS>;
   constexpr size_t smem = sizeof(Smem);
-  auto kern = compress_ws_kernel<C, BF16, KC, IBC, CAP, KMAX, NSW, NSEL, D, NS>;
+  static_assert(smem <= 227 * 1024, "compress_ws shared memory");
+  auto kern = compress_ws_kernel<C, BF16, KC, IBC, CAP, KMAX, VPU, NSW, NSEL, D, NS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0;
@@ -396,15 +440,16 @@ cudaError_t launch_ws_t(const CompressArgs& a, cudaStream_t s) {
   if (grid > a.n_chunks) grid = a.n_chunks;
   kern<<<(unsigned)grid, (NSW + NSEL) * 32, smem, s>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  compress_fallback_kernel<C, BF16, KC, IBC, CAP, KMAX><<<(unsigned)(SLC_FB_MINB * sms), kFbWarps * 32, 0, s>>>(a);
+  compress_fallback_kernel<C, BF16, KC, IBC, CAP, KMAX, VPU><<<(unsigned)(SLC_FB_MINB * sms), kFbWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int C, bool BF16>
 cudaError_t launch_ws_c(const CompressArgs& a, cudaStream_t s) {
   if (C == 4096 && a.g.k == 64 && a.g.ib == 12)  // the paper's geometry
-    return launch_ws_t<C, BF16, 64, 12, SLC_WS_CAP64, 64>(a, s);
-  return launch_ws_t<C, BF16, 0, 0, SLC_WS_CAPG, kMaxK>(a, s);
+    return launch_ws_t<C, BF16, 64, 12, SLC_WS_CAP64, 64, 4>(a, s);
+  if (ws_vpu(a.g) == 1) return launch_ws_t<C, BF16, 0, 0, SLC_WS_CAPG, kMaxK, 1>(a, s);
+  return launch_ws_t<C, BF16, 0, 0, SLC_WS_CAPG, kMaxK, 4>(a, s);
 }
 
 }  // namespace

@@ -458,7 +458,7 @@ slc_status slc_plan_create(const slc_geometry* geom, const slc_tensor* layout, i
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_wire_off, wire_off.size() * sizeof(int64_t));
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_rec_extra, slc::kMaxRecOut * sizeof(uint64_t));
     if (ce == cudaSuccess) ce = cudaMalloc(&p->d_pc_scratch, slc::peer_copy_scratch_bytes());
-    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_defer, slc::defer_words((int64_t)table.size()) * sizeof(uint32_t));
+    if (ce == cudaSuccess) ce = cudaMalloc(&p->d_defer, slc::defer_words(p->g, (int64_t)table.size()) * sizeof(uint32_t));
     if (ce == cudaSuccess) ce = cudaMemset(p->d_defer, 0, slc::kDeferHdr * sizeof(uint32_t));
     if (ce == cudaSuccess)
       ce = cudaMemcpy(p->d_wire_off, wire_off.data(), wire_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
@@ -554,6 +554,7 @@ slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* t
   a.n_extra = p->n_extra_next;
   a.defer = p->d_defer;
   a.defer_cap = p->n_chunks;
+  a.defer_info = slc::defer_info_words(p->g);
   DeviceGuard guard(p->device);
   cudaStream_t st = use_stream(p, stream);
   if (slc::compress_tma_supported(p->g)) {

@@ -78,11 +78,19 @@ struct CompressArgs {
   // words (warp_select.cuh stage_R).
   uint32_t* defer;
   int64_t defer_cap;
+  int32_t defer_info;  // words per deferral info entry (defer_info_words)
 };
 constexpr int kMaxRecOut = 16;
 constexpr int kDeferHdr = 4;
-constexpr int kDeferInfo = 9;  // T, then one group-mask word per pass (NP <= 8)
-inline int64_t defer_words(int64_t n_chunks) { return kDeferHdr + n_chunks * (1 + kDeferInfo); }
+// compress_ws hand-off unit: quads (VPU = 1) when k exceeds a quarter of the
+// 32 NP 16-position groups of a chunk (their maxima then give a weak T),
+// else the groups (VPU = 4; the paper's C = 4096, k = 64)
+inline int ws_vpu(const Geom& g) { return (g.C == 1024 || g.C == 4096) && 4 * g.k > 32 * (g.C / 512) ? 1 : 4; }
+// deferral info entry: T, then one unit-mask ballot word per unit of a lane
+inline int defer_info_words(const Geom& g) { return 1 + (g.C / 512) * 4 / ws_vpu(g); }
+inline int64_t defer_words(const Geom& g, int64_t n_chunks) {
+  return kDeferHdr + n_chunks * (1 + (int64_t)defer_info_words(g));
+}
 
 enum AggMode : int { kAggOnly = 0, kUpdateFromAgg = 1, kFused = 2 };
 

@@ -81,7 +81,17 @@ struct WarpCfg {
 
 // per-warp shared scratch; CAP = candidate capacity (larger sets take the
 // fallback), KMAX = largest k the instantiation serves
-template <int C, int CAP, int KMAX>
+// VPU = 4-position groups (quads) per unit, the span one hand-off maximum
+// covers: 4 (a 16-position group (lane, u); the paper's geometry) or 1 (a quad:
+// NU = 4 NP units per lane, for k close to the 32 NP groups of a chunk)
+template <int C, int VPU>
+struct UnitCfg {
+  static constexpr int NP = C / 512;
+  static constexpr int NU = NP * 4 / VPU;  // units per lane
+  static constexpr int HN = 32 * NU > 256 ? 32 * NU : 256;
+};
+
+template <int C, int CAP, int KMAX, int VPU = 4>
 struct WarpScratch {
   uint64_t cand[CAP];
   float candb[CAP];
@@ -95,10 +105,16 @@ struct WarpScratch {
   };
   uint32_t fb[4];                // stage B -> select_fallback: G, Kmin, M, bad (kept out of registers)
   uint32_t gm[32];               // per lane: bit u = group (lane, u) may hold a selected value (max >= T)
-  uint32_t hist[256];  // fallback histogram; also the group list of stage B (<= 32*NP <= 256 groups)
-  uint32_t selpos[KMAX];
-  float selval[KMAX];
-  uint32_t code[KMAX];
+  union {
+    // the unit list of stage B (<= 32 NU entries) and the fallbacks' histograms,
+    // dead once the slots below are written (R fills them, Q and F read them)
+    uint32_t hist[UnitCfg<C, VPU>::HN];
+    struct {
+      uint32_t selpos[KMAX];
+      float selval[KMAX];
+      uint32_t code[KMAX];
+    };
+  };
   // key_select: candidates held per lane (registers), and so the largest M it serves
   static constexpr int NXK = (CAP + 2 * WarpCfg<C>::BW) / 32 < 16 ? (CAP + 2 * WarpCfg<C>::BW) / 32 : 16;
   static constexpr int XCAP = 32 * NXK;
@@ -169,8 +185,8 @@ __device__ __forceinline__ int nth_set_bit(uint32_t w, int r) {
 // (the largest word whose prefix is <= j holds bit j) and its bit by
 // nth_set_bit; the values are re-read from e (= b) with every lane's load in
 // flight at once (a per-lane walk of its own words serialises on tied rows)
-template <int C, int CAP, int KMAX>
-__device__ __forceinline__ void fill_slots(const float* ef, WarpScratch<C, CAP, KMAX>& ws, const int lane,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __forceinline__ void fill_slots(const float* ef, WarpScratch<C, CAP, KMAX, VPU>& ws, const int lane,
                                            const ChunkDesc& d, const int n_sel) {
   using K = WarpCfg<C>;
   constexpr int WPL = K::BW / 32;
@@ -202,12 +218,12 @@ __device__ __forceinline__ void fill_slots(const float* ef, WarpScratch<C, CAP, 
 #ifndef SLC_RADIX_UB
 #define SLC_RADIX_UB 1  // passes whose loads radix_fallback keeps in flight (measured: 4 spills, slower)
 #endif
-template <int C, int CAP, int KMAX>
-__device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX, VPU>* wsp, const int lane, const ChunkDesc d,
                                             const int len, const bool full, const int k_eff) {
   using K = WarpCfg<C>;
   constexpr int NP = K::NP;
-  WarpScratch<C, CAP, KMAX>& ws = *wsp;
+  WarpScratch<C, CAP, KMAX, VPU>& ws = *wsp;
   // only groups whose maximum reaches T can hold a selected value (>= k_eff
   // values are >= T): the other groups are neither loaded nor counted
   const uint32_t gm = ws.gm[lane];
@@ -230,10 +246,11 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
       bool any = false;
 #pragma unroll
       for (int b = 0; b < UB; b++) {
-        const bool act = u0 + b < NP && ((gm >> (u0 + b)) & 1u);
-        any |= act;
 #pragma unroll
         for (int v = 0; v < 4; v++) {
+          // unit of quad (u, v): u for 16-position groups, 4u + v for quads
+          const bool act = u0 + b < NP && ((gm >> ((4 * (u0 + b) + v) / VPU)) & 1u);
+          any |= act;
           const int q = 128 * (u0 + b) + 32 * v + lane;
           nvs[b][v] = act ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
           load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nvs[b][v], ev[b][v]);
@@ -302,7 +319,8 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
 #pragma unroll
       for (int v = 0; v < 4; v++) {
         const int q = 128 * (u0 + b) + 32 * v + lane;
-        nvs[b][v] = (u0 + b < NP && ((gm >> (u0 + b)) & 1u)) ? (full ? 4 : valid_in_group(4 * q, len)) : 0;
+        nvs[b][v] = (u0 + b < NP && ((gm >> ((4 * (u0 + b) + v) / VPU)) & 1u)) ? (full ? 4 : valid_in_group(4 * q, len))
+                                                                                 : 0;
         load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, q), nvs[b][v], ev[b][v]);
       }
 #pragma unroll
@@ -338,7 +356,7 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
       }
   }
   __syncwarp();
-  fill_slots<C, CAP, KMAX>(ef, ws, lane, d, k_eff);
+  fill_slots<C, CAP, KMAX, VPU>(ef, ws, lane, d, k_eff);
 #ifdef SLC_PHASE_TIMING
   PATH_ADD(6, clock64() - t1);
 #endif
@@ -352,20 +370,20 @@ __device__ __noinline__ void radix_fallback(float* ef, WarpScratch<C, CAP, KMAX>
 // in position order (R#4) — done here.  A >= k_eff: the answer lies among
 // the A candidates (rank them if A <= CAP), else the radix fallback.
 // Returns true when the selection is complete (ws.selpos / selval filled).
-template <int C, int CAP, int KMAX>
-__device__ __forceinline__ bool tie_select(float* ef, WarpScratch<C, CAP, KMAX>& ws, const int lane, const Sel& s,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __forceinline__ bool tie_select(float* ef, WarpScratch<C, CAP, KMAX, VPU>& ws, const int lane, const Sel& s,
                                            int& M) {
 using K = WarpCfg<C>;
-constexpr int NP = K::NP;
+constexpr int NU = UnitCfg<C, VPU>::NU;
 {
   // Kmin: the smallest key >= Tc among the candidate groups (one more L2 pass)
   uint32_t Kc = 0xFFFFFFFFu;
   for (int gi = lane; gi < s.G; gi += 32) {
     const uint32_t id = ws.hist[gi];
-    const int owner = (int)(id / NP), u = (int)(id % NP);
+    const int owner = (int)(id / NU), u = (int)(id % NU);
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
-      const int q = 128 * u + 32 * v + owner;
+    for (int v = 0; v < VPU; v++) {
+      const int q = 32 * (VPU * u + v) + owner;
       const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
       float x[4];
       load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(s.d, q), nv, x);
@@ -382,7 +400,7 @@ constexpr int NP = K::NP;
   int A = 0;
   constexpr int BR = 1;  // one group per lane in flight: the fallback keeps its register footprint small
   for (int r0 = 0; r0 < s.G; r0 += 32 * BR) {
-    float vals[BR][16];
+    float vals[BR][4 * VPU];
     int owner[BR], uu[BR];
 #pragma unroll
     for (int bq = 0; bq < BR; bq++) {
@@ -391,11 +409,11 @@ constexpr int NP = K::NP;
       uu[bq] = 0;
       if (gi < s.G) {
         const uint32_t id = ws.hist[gi];
-        owner[bq] = (int)(id / NP);
-        uu[bq] = (int)(id % NP);
+        owner[bq] = (int)(id / NU);
+        uu[bq] = (int)(id % NU);
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
-          const int q = 128 * uu[bq] + 32 * v + owner[bq];
+        for (int v = 0; v < VPU; v++) {
+          const int q = 32 * (VPU * uu[bq] + v) + owner[bq];
           load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(s.d, q), s.full ? 4 : valid_in_group(4 * q, s.len), &vals[bq][4 * v]);
         }
       }
@@ -406,8 +424,8 @@ constexpr int NP = K::NP;
       uint32_t cmask = 0;
       if (gi < s.G) {
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
-          const int q = 128 * uu[bq] + 32 * v + owner[bq];
+        for (int v = 0; v < VPU; v++) {
+          const int q = 32 * (VPU * uu[bq] + v) + owner[bq];
           const int nv = s.full ? 4 : valid_in_group(4 * q, s.len);
           uint32_t tmask = 0;
 #pragma unroll
@@ -423,9 +441,9 @@ constexpr int NP = K::NP;
       int o = A + warp_excl_scan(cc);
       A += (int)__reduce_add_sync(kFull, (unsigned)cc);
 #pragma unroll
-      for (int j = 0; j < 16; j++) {
+      for (int j = 0; j < 4 * VPU; j++) {
         if ((cmask >> j) & 1u) {
-          const int p = 4 * (128 * uu[bq] + 32 * (j >> 2) + owner[bq]) + (j & 3);
+          const int p = 4 * (32 * (VPU * uu[bq] + (j >> 2)) + owner[bq]) + (j & 3);
           if (o < CAP) {
             ws.cand[o] = ((uint64_t)key2_of(vals[bq][j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
             ws.candb[o] = vals[bq][j];
@@ -464,7 +482,7 @@ constexpr int NP = K::NP;
     if (take) atomicOr(&ws.bit[WPL * lane + x], take);
   }
   __syncwarp();
-  fill_slots<C, CAP, KMAX>(ef, ws, lane, s.d, s.k_eff);
+  fill_slots<C, CAP, KMAX, VPU>(ef, ws, lane, s.d, s.k_eff);
   return true;
 }
 }
@@ -473,8 +491,8 @@ constexpr int NP = K::NP;
 // exact rank of the M <= CAP candidates in ws.cand (key << 16 | ~pos: ties go to
 // the lower position, R#3, R#4); rank < k_eff -> selected; the selection
 // bitmap's prefix gives each its slot in ascending position (R#5)
-template <int C, int CAP, int KMAX>
-__device__ __forceinline__ void rank_select(WarpScratch<C, CAP, KMAX>& ws, const int lane, const int M,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __forceinline__ void rank_select(WarpScratch<C, CAP, KMAX, VPU>& ws, const int lane, const int M,
                                             const int k_eff) {
   constexpr int WPL = WarpCfg<C>::BW / 32;
   const int NM = (M + 31) >> 5;
@@ -549,12 +567,13 @@ __device__ __forceinline__ void rank_select(WarpScratch<C, CAP, KMAX>& ws, const
 #else
 #define SLC_KS_ATTR __noinline__
 #endif
-template <int C, int CAP, int KMAX>
-__device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX, VPU>* wsp, const int lane, const ChunkDesc d,
                                         const int len, const int k_eff, const int G, const uint32_t Tc, const int M) {
   using K = WarpCfg<C>;
-  using WS = WarpScratch<C, CAP, KMAX>;
-  constexpr int NP = K::NP;
+  using WS = WarpScratch<C, CAP, KMAX, VPU>;
+  constexpr int NU = UnitCfg<C, VPU>::NU;
+  constexpr int UPL = 4 / VPU;  // units per lane per L2 round trip of the mark pass
   constexpr int WPL = K::BW / 32;
   constexpr int NXK = WS::NXK;
   WS& ws = *wsp;
@@ -592,29 +611,41 @@ __device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp
   __syncwarp();  // xkey (= tie) read by every lane before it is cleared
   for (int w = lane; w < K::BW; w += 32) ws.tie[w] = 0u;
   __syncwarp();
-  // mark: one pass over the candidate groups (lane gi = group list entry gi)
+  // mark: one pass over the candidate units (lane gi = unit list entry gi)
 #pragma unroll 1
-  for (int gi = lane; gi - lane < G; gi += 32) {
-    if (gi >= G) continue;
-    const uint32_t id = ws.hist[gi];
-    const int qb = 128 * (int)(id % NP) + (int)(id / NP);
-    float x[4][4];
+  for (int g0 = 0; g0 < G; g0 += 32 * UPL) {
+    float x[UPL][VPU][4];
+    int qb[UPL];
 #pragma unroll
-    for (int v = 0; v < 4; v++)
-      load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb + 32 * v), full ? 4 : valid_in_group(4 * (qb + 32 * v), len), x[v]);
+    for (int ub = 0; ub < UPL; ub++) {
+      const int gi = g0 + 32 * ub + lane;
+      qb[ub] = -1;
+      if (gi < G) {
+        const uint32_t id = ws.hist[gi];
+        qb[ub] = 32 * VPU * (int)(id % NU) + (int)(id / NU);
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
-      const int p0 = 4 * (qb + 32 * v);
-      const int nv = full ? 4 : valid_in_group(p0, len);
-      uint32_t mg = 0, me = 0;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const uint32_t kk = j < nv ? key2_of(x[v][j]) : 0u;
-        mg |= (uint32_t)(kk > Ks) << j;
-        me |= (uint32_t)(kk == Ks) << j;
+        for (int v = 0; v < VPU; v++)
+          load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb[ub] + 32 * v),
+                        full ? 4 : valid_in_group(4 * (qb[ub] + 32 * v), len), x[ub][v]);
       }
-      if (mg) atomicOr(&ws.bit[p0 >> 5], mg << (p0 & 31));
-      if (me) atomicOr(&ws.tie[p0 >> 5], me << (p0 & 31));
+    }
+#pragma unroll
+    for (int ub = 0; ub < UPL; ub++) {
+      if (qb[ub] < 0) continue;
+#pragma unroll
+      for (int v = 0; v < VPU; v++) {
+        const int p0 = 4 * (qb[ub] + 32 * v);
+        const int nv = full ? 4 : valid_in_group(p0, len);
+        uint32_t mg = 0, me = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t kk = j < nv ? key2_of(x[ub][v][j]) : 0u;
+          mg |= (uint32_t)(kk > Ks) << j;
+          me |= (uint32_t)(kk == Ks) << j;
+        }
+        if (mg) atomicOr(&ws.bit[p0 >> 5], mg << (p0 & 31));
+        if (me) atomicOr(&ws.tie[p0 >> 5], me << (p0 & 31));
+      }
     }
   }
   __syncwarp();
@@ -636,7 +667,7 @@ __device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp
     }
   }
   __syncwarp();
-  fill_slots<C, CAP, KMAX>(ef, ws, lane, d, k_eff);
+  fill_slots<C, CAP, KMAX, VPU>(ef, ws, lane, d, k_eff);
 }
 
 // ---- more than XCAP candidates (large k against the 32*NP group maxima, so
@@ -649,13 +680,13 @@ __device__ SLC_KS_ATTR void key_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp
 #ifndef SLC_HIST_BR
 #define SLC_HIST_BR 1  // candidate groups per lane per L2 round trip in hist_select's counting pass
 #endif
-template <int C, int CAP, int KMAX>
-__device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane, const ChunkDesc d,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX, VPU>* wsp, const int lane, const ChunkDesc d,
                                          const int len, const int k_eff, const int G, const uint32_t Tc) {
   using K = WarpCfg<C>;
-  using WS = WarpScratch<C, CAP, KMAX>;
-  constexpr int NP = K::NP;
-  constexpr int BR = SLC_HIST_BR;
+  using WS = WarpScratch<C, CAP, KMAX, VPU>;
+  constexpr int NU = UnitCfg<C, VPU>::NU;
+  constexpr int BR = SLC_HIST_BR * 4 / VPU;  // units per lane per L2 round trip
   static_assert(2 * CAP >= 256, "hist_select keeps its histogram in ws.cand");
   WS& ws = *wsp;
   const bool full = len == C;
@@ -667,7 +698,7 @@ __device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* w
   auto walk = [&](auto&& f) {
 #pragma unroll 1
     for (int r0 = 0; r0 < G; r0 += 32 * BR) {
-      float vals[BR][16];
+      float vals[BR][4 * VPU];
       int qb[BR];
 #pragma unroll
       for (int bq = 0; bq < BR; bq++) {
@@ -675,9 +706,9 @@ __device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* w
         qb[bq] = -1;
         if (gi < G) {
           const uint32_t id = ws.hist[gi];
-          qb[bq] = 128 * (int)(id % NP) + (int)(id / NP);
+          qb[bq] = 32 * VPU * (int)(id % NU) + (int)(id / NU);
 #pragma unroll
-          for (int v = 0; v < 4; v++)
+          for (int v = 0; v < VPU; v++)
             load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb[bq] + 32 * v),
                           full ? 4 : valid_in_group(4 * (qb[bq] + 32 * v), len), &vals[bq][4 * v]);
         }
@@ -685,7 +716,7 @@ __device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* w
 #pragma unroll
       for (int bq = 0; bq < BR; bq++) {
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
+        for (int v = 0; v < VPU; v++) {
           const int p0 = 4 * (qb[bq] + 32 * v);
           const int nv = qb[bq] < 0 ? 0 : (full ? 4 : valid_in_group(p0, len));
 #pragma unroll
@@ -725,47 +756,57 @@ __device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* w
   const uint32_t T2 = max(Tc, base + (D << 20));
   __syncwarp();  // the histogram (ws.cand) is read; the candidates overwrite it
   int M = 0;
+  constexpr int UPL = 4 / VPU;
 #pragma unroll 1
-  for (int r0 = 0; r0 < G; r0 += 32) {
-    const int gi = r0 + lane;
-    float vals[16];
-    int qb = -1;
-    uint32_t cmask = 0;
-    if (gi < G) {
-      const uint32_t id = ws.hist[gi];
-      qb = 128 * (int)(id % NP) + (int)(id / NP);
+  for (int r0 = 0; r0 < G; r0 += 32 * UPL) {
+    float vals[UPL][4 * VPU];
+    int qb[UPL];
 #pragma unroll
-      for (int v = 0; v < 4; v++)
-        load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb + 32 * v), full ? 4 : valid_in_group(4 * (qb + 32 * v), len),
-                      &vals[4 * v]);
+    for (int ub = 0; ub < UPL; ub++) {
+      const int gi = r0 + 32 * ub + lane;
+      qb[ub] = -1;
+      if (gi < G) {
+        const uint32_t id = ws.hist[gi];
+        qb[ub] = 32 * VPU * (int)(id % NU) + (int)(id / NU);
 #pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const int nv = full ? 4 : valid_in_group(4 * (qb + 32 * v), len);
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-          if (j < nv && key2_of(vals[4 * v + j]) >= T2) cmask |= 1u << (4 * v + j);
+        for (int v = 0; v < VPU; v++)
+          load_f32x4_l2(ef, goff<K::RPQ_SHIFT>(d, qb[ub] + 32 * v),
+                        full ? 4 : valid_in_group(4 * (qb[ub] + 32 * v), len), &vals[ub][4 * v]);
       }
     }
-    const int cc = __popc(cmask);
-    int o = M + warp_excl_scan(cc);
-    M += (int)__reduce_add_sync(kFull, (unsigned)cc);
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      if ((cmask >> j) & 1u) {
-        const int p = 4 * (qb + 32 * (j >> 2)) + (j & 3);
-        if (o < CAP) {
-          ws.cand[o] = ((uint64_t)key2_of(vals[j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
-          ws.candb[o] = vals[j];
-        } else if (o < WS::XCAP) {
-          ws.xkey[o - CAP] = key2_of(vals[j]);
+    for (int ub = 0; ub < UPL; ub++) {
+      uint32_t cmask = 0;
+      if (qb[ub] >= 0) {
+#pragma unroll
+        for (int v = 0; v < VPU; v++) {
+          const int nv = full ? 4 : valid_in_group(4 * (qb[ub] + 32 * v), len);
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (j < nv && key2_of(vals[ub][4 * v + j]) >= T2) cmask |= 1u << (4 * v + j);
         }
-        o++;
+      }
+      const int cc = __popc(cmask);
+      int o = M + warp_excl_scan(cc);
+      M += (int)__reduce_add_sync(kFull, (unsigned)cc);
+#pragma unroll
+      for (int j = 0; j < 4 * VPU; j++) {
+        if ((cmask >> j) & 1u) {
+          const int p = 4 * (qb[ub] + 32 * (j >> 2)) + (j & 3);
+          if (o < CAP) {
+            ws.cand[o] = ((uint64_t)key2_of(vals[ub][j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
+            ws.candb[o] = vals[ub][j];
+          } else if (o < WS::XCAP) {
+            ws.xkey[o - CAP] = key2_of(vals[ub][j]);
+          }
+          o++;
+        }
       }
     }
   }
   __syncwarp();
   SLC_CHECK(M == M2, "hist_select candidates");
-  key_select<C, CAP, KMAX>(ef, wsp, lane, d, len, k_eff, G, T2, M);
+  key_select<C, CAP, KMAX, VPU>(ef, wsp, lane, d, len, k_eff, G, T2, M);
   return true;
 }
 
@@ -773,8 +814,8 @@ __device__ __noinline__ bool hist_select(float* ef, WarpScratch<C, CAP, KMAX>* w
 // function: the common path keeps its registers).  Returns 0 when ws.selpos /
 // selval are complete, else the number of candidates left in ws.cand (<= CAP)
 // for the exact-rank path.
-template <int C, int CAP, int KMAX>
-__device__ __noinline__ int select_fallback(float* ef, WarpScratch<C, CAP, KMAX>* wsp, const int lane,
+template <int C, int CAP, int KMAX, int VPU>
+__device__ __noinline__ int select_fallback(float* ef, WarpScratch<C, CAP, KMAX, VPU>* wsp, const int lane,
                                             const ChunkDesc d, const int len, const int k_eff) {
   Sel s;
   s.d = d;
@@ -787,26 +828,26 @@ __device__ __noinline__ int select_fallback(float* ef, WarpScratch<C, CAP, KMAX>
   const int M0 = M;
   (void)M0;
   const bool bad = wsp->fb[3] != 0;
-  if (!bad && s.G <= 256 && M <= WarpScratch<C, CAP, KMAX>::XCAP) {
+  if (!bad && s.G <= UnitCfg<C, VPU>::HN && M <= WarpScratch<C, CAP, KMAX, VPU>::XCAP) {
 #ifdef SLC_PHASE_TIMING
     const long long t0 = clock64();
 #endif
-    key_select<C, CAP, KMAX>(ef, wsp, lane, d, len, k_eff, s.G, s.Kmin, M);
+    key_select<C, CAP, KMAX, VPU>(ef, wsp, lane, d, len, k_eff, s.G, s.Kmin, M);
 #ifdef SLC_PHASE_TIMING
     PATH_ADD(10, clock64() - t0);
 #endif
     PATH_COUNT(9);
     return 0;
   }
-  if (!bad && s.G <= 256 && hist_select<C, CAP, KMAX>(ef, wsp, lane, d, len, k_eff, s.G, s.Kmin)) {
+  if (!bad && s.G <= UnitCfg<C, VPU>::HN && hist_select<C, CAP, KMAX, VPU>(ef, wsp, lane, d, len, k_eff, s.G, s.Kmin)) {
     PATH_COUNT(11);
     return 0;
   }
-  if (!bad && s.G <= 256) {
+  if (!bad && s.G <= UnitCfg<C, VPU>::HN) {
 #ifdef SLC_PHASE_TIMING
     const long long t0 = clock64();
 #endif
-    const bool done = tie_select<C, CAP, KMAX>(ef, *wsp, lane, s, M);
+    const bool done = tie_select<C, CAP, KMAX, VPU>(ef, *wsp, lane, s, M);
 #ifdef SLC_PHASE_TIMING
     PATH_ADD(4, clock64() - t0);
 #endif
@@ -816,24 +857,25 @@ __device__ __noinline__ int select_fallback(float* ef, WarpScratch<C, CAP, KMAX>
     }
     if (M <= CAP) {  // the k_eff-th largest key is above the tie: rank the candidates above it
       PATH_COUNT(2);
-      rank_select<C, CAP, KMAX>(*wsp, lane, M, k_eff);
+      rank_select<C, CAP, KMAX, VPU>(*wsp, lane, M, k_eff);
       return 0;
     }
   }
   PATH_COUNT(3);
   PATH_ADD(7, s.G);
   PATH_ADD(8, M0);
-  radix_fallback<C, CAP, KMAX>(ef, wsp, lane, d, len, len == C, k_eff);
+  radix_fallback<C, CAP, KMAX, VPU>(ef, wsp, lane, d, len, len == C, k_eff);
   return 0;
 }
 
 // DEFER: a chunk that leaves the candidate path (M > CAP or non-finite) is
 // appended to a.defer and finished by compress_fallback_kernel (its selection
 // code then stays out of the streaming kernel: registers, i-cache)
-template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, bool DEFER = false>
+template <int C, bool BF16, int KC, int IBC, int CAP, int KMAX, int VPU = 4, bool DEFER = false>
 struct Compressor {
   using K = WarpCfg<C>;
   static constexpr int NP = K::NP;
+  static constexpr int NU = UnitCfg<C, VPU>::NU;  // hand-off maxima (units) per lane
   // fields of CompressArgs held by value (a reference to the kernel's param
   // struct would force the struct into local memory)
   float* ef;
@@ -843,13 +885,14 @@ struct Compressor {
   int n_extra;
   uint32_t* defer;
   int64_t defer_cap;
+  int defer_info;
   Geom g;
   int64_t n_elems, n_chunks;
-  WarpScratch<C, CAP, KMAX>& ws;
+  WarpScratch<C, CAP, KMAX, VPU>& ws;
   int lane;
   int k;
 
-  __device__ __forceinline__ Compressor(const CompressArgs& a, WarpScratch<C, CAP, KMAX>& ws_, int lane_, int k_)
+  __device__ __forceinline__ Compressor(const CompressArgs& a, WarpScratch<C, CAP, KMAX, VPU>& ws_, int lane_, int k_)
       : ef(a.ef),
         records(a.records),
         err(a.err),
@@ -857,6 +900,7 @@ struct Compressor {
         n_extra(a.n_extra),
         defer(a.defer),
         defer_cap(a.defer_cap),
+        defer_info(a.defer_info),
         g(a.g),
         n_elems(a.n_elems),
         n_chunks(a.n_chunks),
@@ -865,10 +909,10 @@ struct Compressor {
         k(k_) {}
 
   // ---- S ---------------------------------------------------------------------------
-  __device__ __forceinline__ void stage_S(Sel& s, const uint32_t (&gk)[NP]) {
+  __device__ __forceinline__ void stage_S(Sel& s, const uint32_t (&gk)[NU]) {
     uint32_t gmaxk = 0;
 #pragma unroll
-    for (int u = 0; u < NP; u++) gmaxk = max(gmaxk, gk[u]);
+    for (int u = 0; u < NU; u++) gmaxk = max(gmaxk, gk[u]);
     s.bad = __reduce_max_sync(kFull, gmaxk) >= 0xFF000001u;  // |b| = inf or NaN somewhere
     if (s.bad && lane == 0) atomicOr(err, kErrNonFinite);
     uint32_t T = 0;
@@ -877,18 +921,20 @@ struct Compressor {
       const uint32_t Tp = T | (1u << bit);
       int cnt = 0;
 #pragma unroll
-      for (int u = 0; u < NP; u++) cnt += gk[u] >= Tp;
+      for (int u = 0; u < NU; u++) cnt += gk[u] >= Tp;
       if ((int)__reduce_add_sync(kFull, (unsigned)cnt) >= s.k_eff) T = Tp;
     }
-    s.Tc = max(T, 1u);
+    // quads hand over keys rounded down to 16 bits: T's low 16 bits are
+    // cleared so that "unit key >= Tc" still keeps every unit holding a key >= Tc
+    s.Tc = max(VPU == 1 ? T & 0xFFFF0000u : T, 1u);
   }
 
   // ---- B ---------------------------------------------------------------------------
   // this lane's candidate groups: bit u = group (lane, u) has max key >= Tc
-  __device__ __forceinline__ uint32_t group_mask(const Sel& s, const uint32_t (&gk)[NP]) const {
+  __device__ __forceinline__ uint32_t group_mask(const Sel& s, const uint32_t (&gk)[NU]) const {
     uint32_t gmask = 0;
 #pragma unroll
-    for (int u = 0; u < NP; u++) gmask |= (uint32_t)(gk[u] >= s.Tc) << u;
+    for (int u = 0; u < NU; u++) gmask |= (uint32_t)(gk[u] >= s.Tc) << u;
     return gmask;
   }
 
@@ -898,21 +944,21 @@ struct Compressor {
     const int gbase = warp_excl_scan(gcnt);
     const int G = (int)__reduce_add_sync(kFull, (unsigned)gcnt);
     int M = 0;
-    if (!s.bad && G <= 256) {
+    if (!s.bad) {
       {
         int o = gbase;
         uint32_t mm = gmask;
         while (mm) {
           const int u = __ffs(mm) - 1;
           mm &= mm - 1;
-          ws.hist[o++] = (uint32_t)(lane * NP + u);
+          ws.hist[o++] = (uint32_t)(lane * NU + u);
         }
       }
       __syncwarp();
       // up to BR groups per lane are re-read at once: one L2 round trip, not BR
-      constexpr int BR = SLC_BR;
+      constexpr int BR = SLC_BR * 4 / VPU;  // the same loads in flight for either unit size
       for (int r0 = 0; r0 < G; r0 += 32 * BR) {
-        float vals[BR][16];
+        float vals[BR][4 * VPU];
         int owner[BR], uu[BR];
 #pragma unroll
         for (int bq = 0; bq < BR; bq++) {
@@ -921,11 +967,11 @@ struct Compressor {
           uu[bq] = 0;
           if (gi < G) {
             const uint32_t id = ws.hist[gi];
-            owner[bq] = (int)(id / NP);
-            uu[bq] = (int)(id % NP);
+            owner[bq] = (int)(id / NU);
+            uu[bq] = (int)(id % NU);
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-              const int q = 128 * uu[bq] + 32 * v + owner[bq];
+            for (int v = 0; v < VPU; v++) {
+              const int q = 32 * (VPU * uu[bq] + v) + owner[bq];
               (DEFER ? load_f32x4 : load_f32x4_l2)(ef, goff<K::RPQ_SHIFT>(s.d, q), s.full ? 4 : valid_in_group(4 * q, s.len),
                          &vals[bq][4 * v]);
             }
@@ -937,8 +983,8 @@ struct Compressor {
           uint32_t cmask = 0;
           if (gi < G) {
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-              const int nv = s.full ? 4 : valid_in_group(4 * (128 * uu[bq] + 32 * v + owner[bq]), s.len);
+            for (int v = 0; v < VPU; v++) {
+              const int nv = s.full ? 4 : valid_in_group(4 * (32 * (VPU * uu[bq] + v) + owner[bq]), s.len);
 #pragma unroll
               for (int j = 0; j < 4; j++)
                 if (j < nv && key2_of(vals[bq][4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
@@ -948,13 +994,13 @@ struct Compressor {
           int o = M + warp_excl_scan(cc);
           M += (int)__reduce_add_sync(kFull, (unsigned)cc);
 #pragma unroll
-          for (int j = 0; j < 16; j++) {
+          for (int j = 0; j < 4 * VPU; j++) {
             if ((cmask >> j) & 1u) {
-              const int p = 4 * (128 * uu[bq] + 32 * (j >> 2) + owner[bq]) + (j & 3);
+              const int p = 4 * (32 * (VPU * uu[bq] + (j >> 2)) + owner[bq]) + (j & 3);
               if (o < CAP) {
                 ws.cand[o] = ((uint64_t)key2_of(vals[bq][j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
                 ws.candb[o] = vals[bq][j];
-              } else if (o < WarpScratch<C, CAP, KMAX>::XCAP) {
+              } else if (o < WarpScratch<C, CAP, KMAX, VPU>::XCAP) {
                 ws.xkey[o - CAP] = key2_of(vals[bq][j]);
               }
               o++;
@@ -990,20 +1036,20 @@ struct Compressor {
   }
 
   // false: the chunk was deferred (DEFER), Q and F are the fallback kernel's.
-  // Deferral entry i: defer[kDeferHdr + i] = chunk; info i (kDeferInfo words
+  // Deferral entry i: defer[kDeferHdr + i] = chunk; info i (defer_info words
   // at defer + kDeferHdr + defer_cap) = Tc (0: non-finite chunk), then word u = the
   // ballot of group (lane, u) being a candidate group.
   __device__ __forceinline__ bool stage_R(const Sel& s, const uint32_t gmask) {
     if (s.M <= CAP) {
       PATH_COUNT(0);
-      rank_select<C, CAP, KMAX>(ws, lane, s.M, s.k_eff);
+      rank_select<C, CAP, KMAX, VPU>(ws, lane, s.M, s.k_eff);
     } else if (DEFER) {
       uint32_t i = 0;
       if (lane == 0) i = atomicAdd(&defer[0], 1u);
       i = __shfl_sync(kFull, i, 0);
-      uint32_t* info = defer + kDeferHdr + defer_cap + (int64_t)i * kDeferInfo;
+      uint32_t* info = defer + kDeferHdr + defer_cap + (int64_t)i * defer_info;
 #pragma unroll
-      for (int u = 0; u < NP; u++) {
+      for (int u = 0; u < NU; u++) {
         const uint32_t wu = __ballot_sync(kFull, (gmask >> u) & 1u);
         if (lane == u) info[1 + u] = wu;
       }
@@ -1013,7 +1059,7 @@ struct Compressor {
       }
       return false;
     } else {
-      select_fallback<C, CAP, KMAX>(ef, &ws, lane, s.d, s.len, s.k_eff);
+      select_fallback<C, CAP, KMAX, VPU>(ef, &ws, lane, s.d, s.len, s.k_eff);
     }
     __syncwarp();
     return true;
@@ -1041,7 +1087,7 @@ struct Compressor {
   }
 
   // all stages, in order, for the chunk in s (whose dense e = b is stored)
-  __device__ __forceinline__ void select(Sel& s, const uint32_t (&gk)[NP]) {
+  __device__ __forceinline__ void select(Sel& s, const uint32_t (&gk)[NU]) {
     PHASE_T0();
     stage_S(s, gk);
     PHASE_MARK(1);
@@ -1065,8 +1111,8 @@ struct Compressor {
     s.Tc = s.bad ? 1u : Tc;
     uint32_t gmask = 0;
 #pragma unroll
-    for (int u = 0; u < NP; u++) gmask |= ((info[1 + u] >> lane) & 1u) << u;
-    if (s.bad) gmask = (1u << NP) - 1u;
+    for (int u = 0; u < NU; u++) gmask |= ((info[1 + u] >> lane) & 1u) << u;
+    if (s.bad) gmask = NU == 32 ? 0xFFFFFFFFu : (1u << NU) - 1u;
     stage_B(s, gmask);
     PHASE_MARK(2);
     stage_R(s, gmask);
