@@ -977,25 +977,31 @@ struct Compressor {
             }
           }
         }
+        // one warp scan per round: the lane's candidates of all BR units
+        uint32_t cmask[BR];
+        int cc = 0;
 #pragma unroll
         for (int bq = 0; bq < BR; bq++) {
           const int gi = r0 + 32 * bq + lane;
-          uint32_t cmask = 0;
+          cmask[bq] = 0;
           if (gi < G) {
 #pragma unroll
             for (int v = 0; v < VPU; v++) {
               const int nv = s.full ? 4 : valid_in_group(4 * (32 * (VPU * uu[bq] + v) + owner[bq]), s.len);
 #pragma unroll
               for (int j = 0; j < 4; j++)
-                if (j < nv && key2_of(vals[bq][4 * v + j]) >= s.Tc) cmask |= 1u << (4 * v + j);
+                if (j < nv && key2_of(vals[bq][4 * v + j]) >= s.Tc) cmask[bq] |= 1u << (4 * v + j);
             }
           }
-          const int cc = __popc(cmask);
-          int o = M + warp_excl_scan(cc);
-          M += (int)__reduce_add_sync(kFull, (unsigned)cc);
+          cc += __popc(cmask[bq]);
+        }
+        int o = M + warp_excl_scan(cc);
+        M += (int)__reduce_add_sync(kFull, (unsigned)cc);
+#pragma unroll
+        for (int bq = 0; bq < BR; bq++) {
 #pragma unroll
           for (int j = 0; j < 4 * VPU; j++) {
-            if ((cmask >> j) & 1u) {
+            if ((cmask[bq] >> j) & 1u) {
               const int p = 4 * (32 * (VPU * uu[bq] + (j >> 2)) + owner[bq]) + (j & 3);
               if (o < CAP) {
                 ws.cand[o] = ((uint64_t)key2_of(vals[bq][j]) << 16) | (uint64_t)(0xFFFFu - (uint32_t)p);
