@@ -197,7 +197,12 @@ slc_status slc_compress_range(slc_plan* plan, int64_t chunk_begin, int64_t n_chu
  *                      ascending peer-id order (median-norm weights).
  * Header checks: magic/version/chunk range -> INVALID_ARGUMENT; differing
  * geometry, base_round or layout_digest -> STALE; duplicate peer ids ->
- * INVALID_ARGUMENT. */
+ * INVALID_ARGUMENT.  Records are device records as slc_compress writes them:
+ * an index >= the chunk length or a non-finite used scale latches
+ * INVALID_DATA, but indices are not re-checked for being strictly increasing
+ * (a repeated index could overflow the exact int32 accumulator) — records
+ * from untrusted peers enter through slc_wire_decode, which rejects them
+ * (S:144). */
 slc_status slc_decode_aggregate(slc_plan* plan, const slc_payload_hdr* hdrs_host,
                                 const void* const* records_dev_host, int32_t R, const float* weights_host,
                                 float* agg_dev, void* stream);
