@@ -99,6 +99,9 @@ struct PipeSmem {
 #ifndef SLC_AGG_GPT
 #define SLC_AGG_GPT 4  // 4-position groups per thread (C/(4*GPT) threads per CTA)
 #endif
+#ifndef SLC_AGG_FUSE2
+#define SLC_AGG_FUSE2 1  // FAST chunks: Delta converted in the dense pass (no pass 2, one barrier less)
+#endif
 
 template <int C>
 struct PipeCfg {
@@ -385,7 +388,7 @@ struct Pipe {
           bad = true;
         }
         if (code & 1u) v = -v;
-        spos[r * kk + 32 * h + lane] = (uint16_t)p;
+        if (!SLC_AGG_FUSE2) spos[r * kk + 32 * h + lane] = (uint16_t)p;
         atomicAdd(&acc32[p], v);
       }
     } else if (mode != 2) {
@@ -473,8 +476,13 @@ struct Pipe {
     // oracle's Delta = (float)(acc * invR) with acc = V * 2^(sh-24) exactly,
     // and 2^(sh-24) * invR is exact, so one fp64 product and one fp32 rounding.
     const double invR = a.invR;
-    if (mode == 0) {
-      const double cs = __dmul_rn(invR, __longlong_as_double((long long)(1023 + sh - 24) << 52));  // exact
+    // FAST: 2^(sh-24) * invR, exact
+    const double cs = __dmul_rn(invR, __longlong_as_double((long long)(1023 + sh - 24) << 52));
+    const bool fuse = SLC_AGG_FUSE2 && mode == 0;  // CTA-uniform
+    if (fuse) {
+      // FAST with the conversion folded into the dense pass: no pass 2, no
+      // barrier, no entry positions — the dense pass reads the int32 sums
+    } else if (mode == 0) {
       SLC_UNROLL(SLC_AGG_UNROLL)
       for (int s = t; s < total; s += NT) {
         const int p = spos[s];
@@ -504,19 +512,33 @@ struct Pipe {
         dlt[p] = __double2float_rn(__dmul_rn(accd[p], invR));
       }
     }
-    __syncthreads();  // Delta complete
+    if (!fuse) __syncthreads();  // Delta complete
 
-    // pass 3: dense, untouched positions hold +0
+    // pass 3: dense, untouched positions hold +0 (fused FAST: Delta of each
+    // nonzero sum here, RN32(RN64(V * cs)) as in pass 2; the sums re-zeroed)
     const float alpha = a.alpha;
+    auto delta4 = [&](int qq, float (&dl)[4]) {
+      if (fuse) {
+        int4* a4 = reinterpret_cast<int4*>(acc32) + qq;
+        const int4 av = *a4;
+        *a4 = make_int4(0, 0, 0, 0);
+        const int vv[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) dl[j] = vv[j] != 0 ? __double2float_rn(__dmul_rn((double)vv[j], cs)) : 0.0f;
+      } else {
+        float4* d4 = reinterpret_cast<float4*>(dlt) + qq;
+        const float4 dv = *d4;
+        *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        dl[0] = dv.x; dl[1] = dv.y; dl[2] = dv.z; dl[3] = dv.w;
+      }
+    };
     if (len == C) {
       int64_t o, stp;
       full_addr<C>(d0, t, o, stp);
 #pragma unroll
       for (int v = 0; v < K::GPT; v++) {
-        float4* d4 = reinterpret_cast<float4*>(dlt) + v * NT + t;
-        const float4 dv = *d4;
-        *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const float dl[4] = {dv.x, dv.y, dv.z, dv.w};
+        float dl[4];
+        delta4(v * NT + t, dl);
         if (MODE == kAggOnly) {
           store_f32x4(a.agg, o + v * stp, 4, dl);
         } else {
@@ -530,10 +552,8 @@ struct Pipe {
 #pragma unroll
       for (int v = 0; v < K::GPT; v++) {
         const int q = v * NT + t;
-        float4* d4 = reinterpret_cast<float4*>(dlt) + q;
-        const float4 dv = *d4;
-        *d4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const float dl[4] = {dv.x, dv.y, dv.z, dv.w};
+        float dl[4];
+        delta4(q, dl);
         const int nv = valid_in_group(4 * q, len);
         if (nv == 0) continue;
         const int64_t off = generic_offset(d0, q, K::RPQ_SHIFT);
