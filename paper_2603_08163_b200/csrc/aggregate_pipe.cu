@@ -311,6 +311,7 @@ struct Pipe {
             emin = min(emin, max(1, e));
             emax = max(emax, max(1, e));
           }
+          if (e == 31) emax = 1 << 20;  // a non-finite scale: the chunk takes WIDE, which checks every entry
         }
         tab[r] = make_int4((int)fw[0], (int)fw[1], (int)fw[2], (int)fw[3]);
       }
@@ -379,10 +380,8 @@ struct Pipe {
         const int4 tb = tab[r];
         const bool hb = (code & 2u) != 0;
         const uint32_t flo = (uint32_t)(hb ? tb.z : tb.x), fhi = (uint32_t)(hb ? tb.w : tb.y);
-        int v = (int)__funnelshift_r(flo, fhi, sh);  // F >> sh, exact
-        bool ok = (fhi >> 31) == 0;
-        if (check_p) ok = ok && (int)p < len;
-        if (!ok) {
+        int v = (int)__funnelshift_r(flo, fhi, sh);  // F >> sh, exact (FAST chunks have finite scales)
+        if (check_p && (int)p >= len) {
           p = 0;
           v = 0;
           bad = true;
