@@ -361,6 +361,10 @@ struct Pipe {
       }
     }
     int* acc32 = reinterpret_cast<int*>(acc);
+    // FAST chunks with at least C/8 entries convert Delta in the dense pass
+    // (C conversions there beat pass 2's per-entry work + barrier only when
+    // enough positions are touched; CTA-uniform)
+    const bool fuse = SLC_AGG_FUSE2 && mode == 0 && 8 * total >= C;
 
     if (mode == 0 && k_eff == kk && (kk & 31) == 0) {
       // pass 1, FAST, full chunk: warp w takes 32-slot units (record r, slots
@@ -387,7 +391,7 @@ struct Pipe {
           bad = true;
         }
         if (code & 1u) v = -v;
-        if (!SLC_AGG_FUSE2) spos[r * kk + 32 * h + lane] = (uint16_t)p;
+        if (!fuse) spos[r * kk + 32 * h + lane] = (uint16_t)p;
         atomicAdd(&acc32[p], v);
       }
     } else if (mode != 2) {
@@ -477,7 +481,6 @@ struct Pipe {
     const double invR = a.invR;
     // FAST: 2^(sh-24) * invR, exact
     const double cs = __dmul_rn(invR, __longlong_as_double((long long)(1023 + sh - 24) << 52));
-    const bool fuse = SLC_AGG_FUSE2 && mode == 0;  // CTA-uniform
     if (fuse) {
       // FAST with the conversion folded into the dense pass: no pass 2, no
       // barrier, no entry positions — the dense pass reads the int32 sums
