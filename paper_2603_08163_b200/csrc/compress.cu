@@ -274,16 +274,6 @@ cudaError_t launch_one(const CompressArgs& a, cudaStream_t s) {
 
 bool compress_supported(int C) { return C == 1024 || C == 4096 || C == 16384; }
 
-cudaError_t launch_compress_simple(const CompressArgs& a, int bf16, cudaStream_t s) {
-  if (a.n_chunks == 0) return cudaSuccess;
-  switch (a.g.C) {
-    case 1024: return bf16 ? launch_one<1024, true>(a, s) : launch_one<1024, false>(a, s);
-    case 4096: return bf16 ? launch_one<4096, true>(a, s) : launch_one<4096, false>(a, s);
-    case 16384: return bf16 ? launch_one<16384, true>(a, s) : launch_one<16384, false>(a, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
 cudaError_t launch_compress(const CompressArgs& a, int bf16, cudaStream_t s) {
   if (a.n_chunks == 0) return cudaSuccess;
   switch (a.g.C) {

@@ -557,11 +557,13 @@ slc_status slc_compress_range(slc_plan* p, int64_t c0, int64_t nc, const void* t
   a.defer_info = slc::defer_info_words(p->g);
   DeviceGuard guard(p->device);
   cudaStream_t st = use_stream(p, stream);
+#ifdef SLC_USE_TMA  // measured history: the TMA-fed ring (compress_tma.cu) is slower than compress_ws
   if (slc::compress_tma_supported(p->g)) {
     cudaError_t e = ensure_tmaps(p, theta, theta_local, ef, st);
     if (e != cudaSuccess) return cuda_status(e, p);
     return cuda_status(slc::launch_compress_tma(a, p->dtype == SLC_BF16, st), p);
   }
+#endif
   return cuda_status(slc::launch_compress(a, p->dtype == SLC_BF16, st), p);
 }
 

@@ -147,7 +147,6 @@ cudaError_t launch_index_decode(const ChunkDesc* chunks, int64_t n_chunks, const
 // launchers (return cudaGetLastError())
 cudaError_t launch_compress(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one CTA per chunk, any compiled C (reference kernel for the pipelined one)
-cudaError_t launch_compress_simple(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // one warp per chunk, no block-level synchronisation (C = 1024, 4096)
 cudaError_t launch_compress_warp(const CompressArgs& a, int param_bf16, cudaStream_t s);
 // persistent warp-specialised CTAs: stream warps + select warps (C = 1024, 4096)

@@ -23,7 +23,9 @@ def build(name, defines):
         rel = os.path.relpath(csrc, ROOT)
         subprocess.check_call(f"git -C {ROOT} archive {revs[0]} {rel} include | tar -x -C {tmp}", shell=True)
         csrc = os.path.join(tmp, rel)
-    srcs = ge.SLC_SOURCES
+    srcs = list(ge.SLC_SOURCES)
+    if any(d.startswith("SLC_USE_TMA") for d in defines):
+        srcs += ge.SLC_TMA_SOURCES
     if revs:
         srcs = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cpp")))
     cmd = [ge.NVCC, *ge.ARCH, *ge.NVFLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
