@@ -104,8 +104,10 @@ __device__ __forceinline__ void store_param4(void* base, int64_t off, int n, con
     uint16_t* p = static_cast<uint16_t*>(base) + off;
     if (n == 4) {
       uint2 u;
-      u.x = (uint32_t)f32_to_bf16_rn_bits(v[0]) | ((uint32_t)f32_to_bf16_rn_bits(v[1]) << 16);
-      u.y = (uint32_t)f32_to_bf16_rn_bits(v[2]) | ((uint32_t)f32_to_bf16_rn_bits(v[3]) << 16);
+      // two values per packed convert (each rounded to nearest even, as one at a time)
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+      u.x = *reinterpret_cast<const uint32_t*>(&lo);
+      u.y = *reinterpret_cast<const uint32_t*>(&hi);
       __stcs(reinterpret_cast<uint2*>(p), u);
     } else {
 #pragma unroll
