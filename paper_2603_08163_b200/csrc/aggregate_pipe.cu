@@ -526,7 +526,8 @@ struct Pipe {
         *a4 = make_int4(0, 0, 0, 0);
         const int vv[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-        for (int j = 0; j < 4; j++) dl[j] = vv[j] != 0 ? __double2float_rn(__dmul_rn((double)vv[j], cs)) : 0.0f;
+        // a zero sum gives +0 (cs > 0), as the untouched dlt of pass 2 does
+        for (int j = 0; j < 4; j++) dl[j] = __double2float_rn(__dmul_rn((double)vv[j], cs));
       } else {
         float4* d4 = reinterpret_cast<float4*>(dlt) + qq;
         const float4 dv = *d4;
