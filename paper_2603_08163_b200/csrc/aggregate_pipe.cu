@@ -164,12 +164,14 @@ __device__ __forceinline__ void load_theta(const void* theta, const Desc& d, int
 
 // Slot of record r in a shared-memory record buffer: SR words (32 for the
 // compile-time layout, else RW).  Default layout (KC = 64, RW = 29 words =
-// 116 B): thread i = 8r + q copies record r — as eight 16-B pieces of the
+// 116 B): record r is copied in 8 parts q — eight 16-B pieces of the
 // 16-B-aligned 128-B window holding it ("wide"; the record then starts
 // o = (29c) & 3 words into the slot) when every record buffer is 16-B aligned
-// and the window stays inside the buffer (not the last chunk), else as 4-B
-// words w with w % 8 == (q + 5) % 8.  Either way thread 8r + 7 copies the
-// scale word (word 28), so it can read it after its own cp.async wait.
+// and the window stays inside the buffer (not the last chunk), else 4-B words
+// w with w % 8 == (q + 5) % 8.  Part 7 holds the scale word (word 28); it is
+// copied by thread r (mod NT), the other parts by threads R + 7r + q, so the
+// scale tables are built by the first R threads (one warp at R <= 32) right
+// after their own cp.async wait, without a barrier.
 template <int KC>
 __device__ __forceinline__ bool wide_window(const AggArgs& a, int64_t c) {
   return KC == 64 && a.rec_al16 && c + 1 < a.n_chunks;
@@ -181,12 +183,12 @@ __device__ __forceinline__ void issue_records(const AggArgs& a, int64_t c, uint3
     if (wide_window<KC>(a, c)) {
       const int64_t wstart = (c * RW * 4) & ~(int64_t)15;
       for (int i = t; i < a.R * 8; i += NT) {
-        const int r = i >> 3, q = i & 7;
+        const int r = i < a.R ? i : (i - a.R) / 7, q = i < a.R ? 7 : (i - a.R) % 7;
         cp_async16(srec + r * 32 + q * 4, reinterpret_cast<const char*>(a.rec[r]) + wstart + 16 * q);
       }
     } else {
       for (int i = t; i < a.R * 8; i += NT) {
-        const int r = i >> 3, q = i & 7;
+        const int r = i < a.R ? i : (i - a.R) / 7, q = i < a.R ? 7 : (i - a.R) % 7;
         const uint32_t* rec = a.rec[r] + c * RW;
         for (int w = (q + 5) & 7; w < RW; w += 8) cp_async4(srec + r * 32 + w, rec + w);
       }
@@ -256,12 +258,12 @@ struct Pipe {
     const int k_eff = max(1, (kk * len) / C);
     const int total = a.R * k_eff;
     cp_async_wait1();
-    const bool owner = KC ? (t & 7) == 7 : (t & 31) == (RW - 1) % 32;
+    const bool owner = KC ? t < a.R : (t & 31) == (RW - 1) % 32;
     if (a.weighted && owner) {
       // weighted: the exact products w_r * S_b (35 significant bits) as M * 2^E,
       // M < 2^35; hi word = M >> 32 | (E + 1024) << 8 | sign(w) << 30
       int emin = 0x7FFFFFFF, emax = (int)0x80000000;
-      for (int r = KC ? (t >> 3) : (t >> 5); r < a.R; r += KC ? NT / 8 : NT / 32) {
+      for (int r = KC ? t : (t >> 5); r < a.R; r += KC ? NT : NT / 32) {
         const uint32_t sw = srec[r * SR + RW - 1];
         const float wf = (float)peer_weight(a, r);
         uint32_t fw[4];
@@ -297,7 +299,7 @@ struct Pipe {
       // this thread copied the scale word of records r (issue_records), so it
       // may read them without a barrier: F = fp16 scale as a multiple of 2^-24
       int emin = 31, emax = 0;
-      for (int r = KC ? (t >> 3) : (t >> 5); r < a.R; r += KC ? NT / 8 : NT / 32) {
+      for (int r = KC ? t : (t >> 5); r < a.R; r += KC ? NT : NT / 32) {
         const uint32_t sw = srec[r * SR + RW - 1];
         uint32_t fw[4];
 #pragma unroll
