@@ -92,6 +92,9 @@ struct PipeSmem {
 #ifndef SLC_AGG_MINB
 #define SLC_AGG_MINB 3  // CTAs per SM the register budget is sized for (C = 4096)
 #endif
+#ifndef SLC_AGG_MINB_BF16
+#define SLC_AGG_MINB_BF16 4  // the same with bf16 theta (half the theta registers: 64 suffice)
+#endif
 
 #ifndef SLC_AGG_THETA_NOW
 #define SLC_AGG_THETA_NOW 0  // 1: theta loaded at the start of its own step (single register buffer)
@@ -109,6 +112,7 @@ struct PipeCfg {
   static constexpr int NT = C / (4 * GPT);
   static constexpr int MIN_BLOCKS = GPT == 4 ? ((C == 4096) ? SLC_AGG_MINB : 4 * SLC_AGG_MINB)
                                             : ((C == 4096) ? 4 : 16);
+  static constexpr int MIN_BLOCKS_BF16 = (GPT == 4 && C == 4096) ? SLC_AGG_MINB_BF16 : MIN_BLOCKS;
   static constexpr int RPQ = ChunkCfg<C>::RPQ;  // 4-element groups per block row
   static constexpr int RPQ_SHIFT = (RPQ == 8) ? 3 : (RPQ == 16 ? 4 : 5);
 };
@@ -592,7 +596,8 @@ struct Pipe {
 };
 
 template <int C, bool BF16, int MODE, int KC>
-__global__ void __launch_bounds__(PipeCfg<C>::NT, PipeCfg<C>::MIN_BLOCKS) agg_pipe_kernel(const AggArgs a) {
+__global__ void __launch_bounds__(PipeCfg<C>::NT, BF16 ? PipeCfg<C>::MIN_BLOCKS_BF16 : PipeCfg<C>::MIN_BLOCKS)
+    agg_pipe_kernel(const AggArgs a) {
   using S = PipeSmem<C>;
   constexpr int NT = PipeCfg<C>::NT;
   extern __shared__ __align__(16) unsigned char smem[];
