@@ -102,6 +102,9 @@ struct PipeSmem {
 #ifndef SLC_AGG_GPT
 #define SLC_AGG_GPT 4  // 4-position groups per thread (C/(4*GPT) threads per CTA)
 #endif
+#ifndef SLC_AGG_FUSE_MUL
+#define SLC_AGG_FUSE_MUL 64  // fuse when R * k_eff >= C / SLC_AGG_FUSE_MUL (measured: 64 beats 8 at R = 2-4, ties elsewhere)
+#endif
 #ifndef SLC_AGG_FUSE2
 #define SLC_AGG_FUSE2 1  // FAST chunks: Delta converted in the dense pass (no pass 2, one barrier less)
 #endif
@@ -367,10 +370,10 @@ struct Pipe {
       }
     }
     int* acc32 = reinterpret_cast<int*>(acc);
-    // FAST chunks with at least C/8 entries convert Delta in the dense pass
+    // FAST chunks with at least C/64 entries convert Delta in the dense pass
     // (C conversions there beat pass 2's per-entry work + barrier only when
     // enough positions are touched; CTA-uniform)
-    const bool fuse = SLC_AGG_FUSE2 && mode == 0 && 8 * total >= C;
+    const bool fuse = SLC_AGG_FUSE2 && mode == 0 && SLC_AGG_FUSE_MUL * total >= C;
 
     if (mode == 0 && k_eff == kk && (kk & 31) == 0) {
       // pass 1, FAST, full chunk: warp w takes 32-slot units (record r, slots
