@@ -102,6 +102,9 @@ struct PipeSmem {
 #ifndef SLC_AGG_GPT
 #define SLC_AGG_GPT 4  // 4-position groups per thread (C/(4*GPT) threads per CTA)
 #endif
+#ifndef SLC_AGG_WTAB
+#define SLC_AGG_WTAB 1  // WFAST: per-record summand table instead of per-entry shifts
+#endif
 #ifndef SLC_AGG_FUSE_MUL
 #define SLC_AGG_FUSE_MUL 64  // fuse when R * k_eff >= C / SLC_AGG_FUSE_MUL (measured: 64 beats 8 at R = 2-4, ties elsewhere)
 #endif
@@ -370,6 +373,30 @@ struct Pipe {
       }
     }
     int* acc32 = reinterpret_cast<int*>(acc);
+    const bool wtab = SLC_AGG_WTAB && mode == 3;  // CTA-uniform
+    if (wtab) {
+      // WFAST: each record's two signed summands (M << (E - Emin), split
+      // lo / hi at Lw bits, the weight's sign applied) once per record here
+      // instead of once per entry; then one barrier
+      for (int r = t; r < a.R; r += NT) {
+        const int4 tb = tab[r];
+        const uint32_t fw[4] = {(uint32_t)tb.x, (uint32_t)tb.y, (uint32_t)tb.z, (uint32_t)tb.w};
+        int out[4];
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          const uint32_t flo = fw[2 * b], fhi = fw[2 * b + 1];
+          const unsigned long long M = ((unsigned long long)(fhi & 0xFFu) << 32) | flo;
+          const int E = (int)((fhi >> 8) & 0xFFFu) - 1024;
+          const unsigned long long v = M ? M << (E - sh) : 0ull;  // < 2^(52 - rbits)
+          int lo = (int)(v & ((1ull << Lw) - 1)), hi = (int)(v >> Lw);
+          if ((fhi >> 30) & 1u) { lo = -lo; hi = -hi; }
+          out[2 * b] = lo;
+          out[2 * b + 1] = hi;
+        }
+        tab[r] = make_int4(out[0], out[1], out[2], out[3]);
+      }
+      __syncthreads();
+    }
     // FAST chunks with at least C/64 entries convert Delta in the dense pass
     // (C conversions there beat pass 2's per-entry work + barrier only when
     // enough positions are touched; CTA-uniform)
@@ -434,7 +461,7 @@ struct Pipe {
         const int4 tb = tab[r];
         const uint32_t flo = (uint32_t)((code & 2u) ? tb.z : tb.x);
         const uint32_t fhi = (uint32_t)((code & 2u) ? tb.w : tb.y);
-        const bool ok = !(fhi >> 31) && !(check_p && (int)p >= len);
+        const bool ok = (wtab || !(fhi >> 31)) && !(check_p && (int)p >= len);
         bad |= !ok;
         if (!ok) p = 0;
         spos[s] = (uint16_t)p;
@@ -442,6 +469,11 @@ struct Pipe {
           int v = ok ? (int)__funnelshift_r(flo, fhi, sh) : 0;  // F >> sh, exact
           if (code & 1u) v = -v;
           atomicAdd(&acc32[p], v);
+        } else if (wtab) {
+          int lo = ok ? (int)flo : 0, hi = ok ? (int)fhi : 0;
+          if (code & 1u) { lo = -lo; hi = -hi; }
+          atomicAdd(&acc32[p], lo);
+          atomicAdd(&acc32[C + p], hi);
         } else if (mode == 3) {
           const unsigned long long M = ((unsigned long long)(fhi & 0xFFu) << 32) | flo;
           const int E = (int)((fhi >> 8) & 0xFFFu) - 1024;
