@@ -26,7 +26,10 @@
  *    overflows) are LATCHED in the plan and reported by slc_get_status(); the
  *    outputs of the offending call are then unspecified.
  *  - Allocations are made only by slc_plan_create (device chunk table, wire
- *    offsets and error word) and by slc_plan_set_option(SLC_OPT_INDEX_CODE)
+ *    offsets, error word, and the compress deferral list: 4 + n_chunks * (2 +
+ *    units per lane) 32-bit words, 40 B per chunk at the paper's geometry —
+ *    chunks whose selection leaves the candidate path are finished by a second
+ *    kernel of the same call) and by slc_plan_set_option(SLC_OPT_INDEX_CODE)
  *    (the f4 binomial table); slc_plan_destroy releases them.
  */
 #ifndef SLC_H
