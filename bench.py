@@ -390,9 +390,12 @@ def run_slc(args):
                                   "north_star's roofline is 8 TB/s per GPU"},
         "kernels": {"compress_ms": ms_compress, "fused_update_ms": ms_update,
                     "compress_bytes_per_launch": comp_bytes, "update_bytes_per_launch": upd_bytes},
-        "gpu_launches": ((4 if args.median_norm else 2)
-                         + (len(offload.pieces) - 1 if offload is not None and args.ef_offload == "pipelined"
-                            else 0)) * args.steps,
+        # per step: compress = the warp-specialised kernel + the deferred-chunk
+        # fallback kernel (C 1024 / 4096; one kernel at C 16384), per piece when
+        # pipelined; then payload norms + weights (median-norm) + the fused update
+        "gpu_launches": ((2 if plan.geom.block * plan.geom.block in (1024, 4096) else 1)
+                         * (len(offload.pieces) if offload is not None and args.ef_offload == "pipelined" else 1)
+                         + (3 if args.median_norm else 1)) * args.steps,
         "clocks": clk.summary(),
     }
     if args.index_code:
